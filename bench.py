@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""bench.py -- end-to-end HistRetinex enhancement throughput on B200 (BASELINE.json metric).
+
+Metric: megapixels/s of end-to-end enhancement (RGB8 -> histograms -> Algorithm 1 solve ->
+gamma target -> LUT -> enhanced RGB8) on 1 B200, plus the fraction of the HBM roofline at
+9 B/pixel (3 B histogram read + 3 B apply read + 3 B apply write).
+
+Default workload: config C3 (64 x 1920x1080 synthetic low-light RGB8 images, per-image seeds),
+the batched configuration the north star's ">= 70% of HBM roofline" target is stated on
+(DESIGN.md section 7 says why C3 and not the single-image configs).  `--config C5` selects the
+other batched config.  Inputs (398 MB) are larger than the 126 MB L2, so no flush is needed
+between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C5|...] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): every rank enhances its own batch (weak scaling, no
+data-path collective -- images are independent); the step time is the max over ranks
+(all_reduce MAX of the device-event time).  `--impl reference` times the CPU oracle (the only
+reference this paper-only tier has) on the host cores; only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+BYTES_PER_PX = 9  # algorithmic minimum: 3 B read (hist) + 3 B read + 3 B write (apply)
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback, used only if no MEASURED_PEAKS.json
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines: list[str] = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(cfg: str, x, p_oracle, budget_s: float = 20.0):
+    """Time the oracle (as it stands) on a bounded sample of the workload on the host cores.
+    Returns (MP/s, cores, description)."""
+    import oracle
+
+    cores = cpu_cores()
+    B = x.shape[0]
+    # one image on one core to size the sample
+    t0 = time.perf_counter()
+    oracle.enhance_batch(x[:1], p_oracle, nthreads=1, want_out=True)
+    t1 = time.perf_counter() - t0
+    n = max(1, min(B, cores, int(budget_s * cores / max(t1, 1e-3) / 2)))
+    th = min(n, cores)
+    t0 = time.perf_counter()
+    oracle.enhance_batch(x[:n], p_oracle, nthreads=th, want_out=True)
+    dt = time.perf_counter() - t0
+    px = n * x.shape[1] * x.shape[2]
+    return px / dt / 1e6, th, f"{n} of {B} images of {cfg} ({x.shape[2]}x{x.shape[1]}), {th} threads, {dt:.2f} s"
+
+
+def run_reference(args, rank):
+    """--impl reference: the CPU oracle (paper-only tier's reference arm) on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    import synth
+
+    cfg = synth.CONFIGS[args.config]
+    cores = cpu_cores()
+    n = max(1, min(cfg.B, cores))
+    x = synth.make_config(args.config, batch=n)
+    p = oracle.Params(use_epsilon=cfg.use_epsilon)
+    # each step: the n-image bounded sample through the whole pipeline, n threads
+    for _ in range(args.warmup):
+        oracle.enhance_batch(x[:1], p, nthreads=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.enhance_batch(x, p, nthreads=n)
+    dt = time.perf_counter() - t0
+    px = args.steps * n * cfg.H * cfg.W
+    v = px / dt / 1e6
+    line = {
+        "impl": "reference", "metric": "megapixels/sec end-to-end enhancement", "value": round(v, 3),
+        "unit": "MP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8+f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg.note}", "images_per_step": n, "H": cfg.H, "W": cfg.W},
+        "cpu_baseline": {"value": round(v, 3), "unit": "MP/s", "cores": n, "kind": "oracle",
+                         "sample": f"{n} of {cfg.B} images of {args.config} per step, {n} host threads"},
+        "e2e": {"value": round(v, 3), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_2510_21100_b200 as hr
+    import synth
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.config]
+    B, H, W = cfg.B, cfg.H, cfg.W
+    params = hr.Params(use_epsilon=cfg.use_epsilon)
+
+    # seeded synthetic batch, generated straight into pinned host memory
+    x_pin = torch.empty((B, H, W, 3), dtype=torch.uint8, pin_memory=True)
+    synth.make_config(args.config, out=x_pin.numpy())
+    x = x_pin.to(dev)
+    out = torch.empty_like(x)
+    out_pin = torch.empty_like(x_pin, pin_memory=True)
+    ws = torch.empty(hr.workspace_bytes(B, H, W), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        hr.hr_enhance(x, params, out=out, workspace=ws)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- device-resident timed region ----
+    hr.profile_enable(local, True)
+    hr.profile_collect(local)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    (hist_ms, solve_ms, apply_ms), nsteps = hr.profile_collect(local)
+    hr.profile_enable(local, False)
+    hist_ms /= max(nsteps, 1)
+    solve_ms /= max(nsteps, 1)
+    apply_ms /= max(nsteps, 1)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end to end through the C-ABI with host buffers (H2D + enhance + D2H per step) ----
+    e2e = None
+    if not args.no_e2e:
+        def step_e2e():
+            x.copy_(x_pin, non_blocking=True)
+            hr.hr_enhance(x, params, out=out, workspace=ws)
+            out_pin.copy_(out, non_blocking=True)
+
+        for _ in range(2):
+            step_e2e()
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        e0.record(stream)
+        ne = max(3, min(args.steps, 10))
+        for _ in range(ne):
+            step_e2e()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = e0.elapsed_time(e1) / ne
+        if dist:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": round(world * B * H * W / (ems / 1e3) / 1e6, 1), "unit": "MP/s",
+               "h2d_bytes_per_step": B * H * W * 3, "d2h_bytes_per_step": B * H * W * 3,
+               "ms_per_step": round(ems, 3),
+               "note": "pinned host -> device copy, hr_enhance, device -> pinned host copy, one stream"}
+
+    px_step = world * B * H * W
+    value = px_step / (ms / 1e3) / 1e6
+    peak, peak_src = peaks()
+    e2e_frac = BYTES_PER_PX * (B * H * W) / (ms / 1e3) / 1e9 / peak
+    # dominant kernel (HBM-bound): the larger of the two streaming kernels
+    kern = {"k_hist": (hist_ms, 3 * B * H * W), "k_apply": (apply_ms, 6 * B * H * W)}
+    name = max(kern, key=lambda k: kern[k][0])
+    kms, kbytes = kern[name]
+    achieved = kbytes / (kms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get(name)
+        except Exception:
+            traffic = None
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        v, cores, sample = oracle_sample(args.config, x_pin.numpy(),
+                                         oracle.Params(use_epsilon=cfg.use_epsilon))
+        cpu_base = {"value": round(v, 3), "unit": "MP/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "megapixels/sec end-to-end enhancement on 1 B200; % of HBM roofline",
+            "value": round(value, 1), "unit": "MP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8+f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg.note}", "batch_per_gpu": B, "H": H, "W": W,
+                       "global_batch": world * B, "parallelism": f"dp{world} (independent images)",
+                       "l2": "inputs larger than L2 (%.0f MB > 126 MB), no flush" % (B * H * W * 3 / 1e6),
+                       "params": {"alpha": params.alpha, "beta": params.beta, "gamma": params.gamma,
+                                  "T": params.max_iter, "use_epsilon": params.use_epsilon,
+                                  "grad_norm": "MAXNORM"}},
+            "hbm_roofline_frac_e2e": round(e2e_frac, 4),
+            "roofline": {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": kbytes},
+            "stages_ms": {"hist": round(hist_ms, 4), "solve": round(solve_ms, 4), "apply": round(apply_ms, 4),
+                          "hist_GBs": round(3 * B * H * W / (hist_ms / 1e3) / 1e9, 1),
+                          "apply_GBs": round(6 * B * H * W / (apply_ms / 1e3) / 1e9, 1),
+                          "solve_us_per_image": round(solve_ms * 1e3 / B, 3)},
+            "cpu_baseline": cpu_base,
+            "e2e": e2e,
+            "clocks": clk,
+            "gpu_launches": 3 * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,157 @@
+/*
+ * histretinex.h -- C-ABI of the B200-native HistRetinex hot path (sm_100a).
+ *
+ * The library computes, for a batch of 8-bit RGB low-light images, the per-image
+ * pipeline of HistRetinex (arXiv 2510.21100, /root/reference/PAPER.md, "P:<line>"):
+ *
+ *   RGB8 -> value channel S and gradient image -> 256-bin count histograms (Eq. 3)
+ *        -> histogram-domain Retinex solve, Algorithm 1 (Eqs. 6-15)
+ *        -> gamma-reprocessed enhanced histogram (Eqs. 17-20)
+ *        -> histogram matching LUT -> per-pixel LUT apply + colour.
+ *
+ * Readings of the paper where it is silent or garbled are DESIGN.md section 3
+ * (R1..R21); they are named at each entry point below.
+ *
+ * Conventions for every call
+ * --------------------------
+ *  - Pointers named *_dev / device arrays are CUDA device pointers owned by the
+ *    caller; the library never allocates caller-visible memory and never frees
+ *    caller memory.  Host pointers appear only in hr_enhance_host.
+ *  - Images are contiguous uint8 [B][H][W][3] (HWC, RGB), per-image stride
+ *    H*W*3 bytes.  Any base alignment is accepted; 16-byte aligned bases with
+ *    W % 16 == 0 take the vectorised path.
+ *  - Histograms are uint32 [B][256]; raw gradient histograms uint32 [B][512]
+ *    (bins 0..510 used, bin 511 always 0).  Float histograms are double [B][256].
+ *  - `stream` is a cudaStream_t (passed as void* so this header needs no CUDA
+ *    include); NULL means the legacy default stream.  All device calls are
+ *    asynchronous on `stream`; they never synchronise the host.
+ *  - Validation is synchronous and happens before anything is launched: on any
+ *    error nothing is enqueued and the status is returned.  Asynchronous CUDA
+ *    faults surface on a later call or on stream synchronisation.
+ *  - Outputs are bit-identical run to run (deterministic reductions, integer
+ *    histogram atomics only).
+ *  - A context is not thread-safe: use one hr_ctx per host thread.
+ *  - No C++ exception or exit() crosses this boundary.
+ */
+#ifndef HISTRETINEX_H
+#define HISTRETINEX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HR_OK = 0,
+  HR_EINVAL = 1,        /* null pointer, B < 1, negative size, parameter out of range */
+  HR_EEMPTY = 2,        /* H*W == 0 (an image has no pixels) */
+  HR_EDEGENERATE = 3,   /* all-zero target histogram in hr_match (per image, see img_status) */
+  HR_ECUDA = 4,         /* a CUDA runtime call failed; text in hr_last_error() */
+  HR_EUNSUPPORTED = 5   /* valid for the paper but not for this build (levels != 256) */
+} hr_status;
+
+/* Parameters of Algorithm 1 ("Input: ... error threshold eps, maximum iteration T,
+   weight parameter alpha and beta") and of the reprocessing (Eq. 17 gamma). */
+typedef struct hr_params {
+  int32_t levels;      /* number of gray levels l; must be 256 (HR_EUNSUPPORTED otherwise) */
+  int32_t max_iter;    /* T >= 1 (Alg. 1); the paper's timing runs use 10 */
+  double alpha;        /* > 0, weight of the illumination prior (Eq. 10) */
+  double beta;         /* > 0, weight of the reflectance (gradient) prior (Eq. 10) */
+  double gamma;        /* >= 1, Eq. 17 gamma on the illumination location vector (R13) */
+  double epsilon;      /* > 0, stop threshold RELATIVE to N^2: ||dh||^2 <= epsilon*N^2 (R11) */
+  int32_t use_epsilon; /* 0: exactly max_iter iterations; 1: Alg. 1 stop rule (R11) */
+  int32_t update_form; /* 0: gradient-consistent Eqs. 12-13 (R7, default); 1: as printed */
+  int32_t grad_norm;   /* 0: MAXNORM gradient levels (R14, default); 1: RAW_CLAMP min(g,255) */
+  int32_t reserved;    /* must be 0 */
+} hr_params;
+
+/* Fills the defaults: levels 256, T 10, alpha 0.1, beta 1e-3, gamma 2.2, epsilon 1e-3,
+   use_epsilon 0, update_form 0, grad_norm 0 (R12-R14).  HR_EINVAL on NULL. */
+hr_status hr_default_params(hr_params* p);
+
+typedef struct hr_ctx hr_ctx;
+
+/* Creates a context bound to CUDA device `device` (queries SM count, L2 size; builds no
+   tables).  *ctx is set to NULL on failure. */
+hr_status hr_create(hr_ctx** ctx, int device);
+/* Destroys a context (NULL is a no-op).  Does not synchronise caller streams. */
+hr_status hr_destroy(hr_ctx* ctx);
+
+const char* hr_status_string(hr_status s);
+/* Last error text of this context (never NULL; "" when none). */
+const char* hr_last_error(const hr_ctx* ctx);
+/* Library version string, e.g. "histretinex-b200 0.1 sm_100a". */
+const char* hr_version(void);
+
+/* Device workspace bytes needed by hr_enhance / hr_histogram / hr_solve for a batch
+   of B images of H x W (0 on invalid sizes).  The caller allocates it (e.g. torch). */
+size_t hr_workspace_bytes(int64_t B, int32_t H, int32_t W);
+
+/* Step (1): value channel S = max(R,G,B) ("S is the value channel ... in the HSV";
+   R15) and its gradient image g = |dx| + |dy| with forward differences, 0 on the last
+   column / row (R14), reduced to count histograms (Eq. 3):
+     hist_s[b][v]     = #{pixels of image b with S == v}                 (256 bins)
+     hist_g_raw[b][g] = #{pixels of image b with raw gradient == g}      (512 slots)
+     hist_g[b][k]     = #{pixels whose gradient level is k}              (256 bins)
+   where the gradient level is MAXNORM: (510*g + gmax) / (2*gmax) (integer division,
+   gmax = largest raw gradient of the image, all 0 if gmax == 0) or RAW_CLAMP: min(g,255),
+   chosen by grad_norm (0/1).  hist_g_raw may be NULL.  Sums equal H*W exactly.
+   Workspace: hr_workspace_bytes(B,H,W) bytes, device. */
+hr_status hr_histogram(hr_ctx* ctx, const uint8_t* rgb_dev, int64_t B, int32_t H, int32_t W,
+                       int32_t grad_norm, uint32_t* hist_s_dev, uint32_t* hist_g_dev,
+                       uint32_t* hist_g_raw_dev, void* ws_dev, void* stream);
+
+/* Step (2): Algorithm 1 on each image's histograms, fp64:
+   H_C(R)^0 = hist_g, H_C(L)^0 = hist_s (R9); repeat Eq. 13, Eq. 12 (raw new R, frozen K,
+   R10), Eq. 15, Eq. 14, Eq. 11 until the stop rule (R11).  Then Eqs. 17-20 give the
+   enhanced histogram target[b][k] = sum over index_1(i,j)==k of hR_i hL_j / N (N = sum
+   hist_s).  Outputs (device, [B][256] doubles; iters [B] nullable): final hL, hR
+   (renormalised, sum N, exactly 0 off the supports of hist_s / hist_g), target.
+   Images with N == 0 get all-zero outputs and iters 0.
+   Workspace: hr_workspace_bytes(B,1,1) bytes or more, device. */
+hr_status hr_solve(hr_ctx* ctx, const uint32_t* hist_s_dev, const uint32_t* hist_g_dev, int64_t B,
+                   const hr_params* params, double* hL_dev, double* hR_dev, double* target_dev,
+                   int32_t* iters_dev, void* ws_dev, void* stream);
+
+/* Step (3): histogram matching (R16).  Cs(v) = Ps(v)/N with Ps the integer prefix
+   of hist_s; Pt(k) = Pt(k-1) + target(k) (plateau-preserving), Ct(k) = Pt(k)/Pt(255);
+   lut[b][v] = smallest k minimising |Ct(k) - Cs(v)| (monotone non-decreasing in v).
+   img_status[b] (nullable) = HR_OK, or HR_EDEGENERATE when Pt(255) <= 0 or N == 0 (lut
+   is then the identity). */
+hr_status hr_match(hr_ctx* ctx, const uint32_t* hist_s_dev, const double* target_dev, int64_t B,
+                   uint8_t* lut_dev, int32_t* img_status_dev, void* stream);
+
+/* Step (4): per-pixel LUT application and colour reconstruction (R17):
+   V = max(R,G,B), V' = lut[b][V]; each channel c -> floor((2*c*V' + V) / (2*V)), i.e.
+   V replaced in exact hexcone HSV with H and S kept, rounded half up; V == 0 -> (V',V',V').
+   rgb_out may equal rgb_in (in place). */
+hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_dev, int64_t B,
+                   int32_t H, int32_t W, uint8_t* rgb_out_dev, void* stream);
+
+/* Steps (1)-(4) for the whole batch ("matching its histogram with the one provided by
+   HistRetinex"), enqueued as one CUDA graph per (shape, params, pointers) on `stream`.
+   Optional debug outputs (device, nullable): hist_s [B][256], lut [B][256], iters [B].
+   rgb_out must not alias rgb_in.  Workspace: hr_workspace_bytes(B,H,W), device. */
+hr_status hr_enhance(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H, int32_t W,
+                     const hr_params* params, uint8_t* rgb_out_dev, void* ws_dev, void* stream);
+
+hr_status hr_enhance_debug(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H,
+                           int32_t W, const hr_params* params, uint8_t* rgb_out_dev, void* ws_dev,
+                           uint32_t* hist_s_dev, uint8_t* lut_dev, int32_t* iters_dev,
+                           void* stream);
+
+/* Stage timing (measurement only).  While enabled, every hr_enhance records four CUDA
+   events on its stream: before the histogram kernel, after it, after the solver, after the
+   apply kernel.  hr_profile_collect waits for the recorded events, returns the summed
+   milliseconds of the three stages (stage_ms[0] histogram incl. its memsets, [1] solve +
+   LUT, [2] apply) over the *steps calls since the last collect, and resets the counters.
+   At most 4096 calls are kept between collects (HR_EINVAL beyond). */
+hr_status hr_profile_enable(hr_ctx* ctx, int32_t on);
+hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HISTRETINEX_H */

@@ -1,0 +1,217 @@
+"""paper_2510_21100_b200 -- B200-native HistRetinex hot path (arXiv 2510.21100).
+
+Thin Python binding over the C-ABI in include/histretinex.h.  Each function has the name
+of the C entry point it calls and only marshals arguments: every step of the path runs in
+the library's sm_100a kernels; there is no CPU fallback (a missing library or a non-CUDA
+tensor raises).  PyTorch is used for device memory and the current CUDA stream.
+
+    out = hr_enhance(x_u8_cuda[B, H, W, 3], Params(gamma=2.2))
+    hist_s, hist_g, hist_g_raw = hr_histogram(x)
+    hL, hR, target, iters = hr_solve(hist_s, hist_g, params)
+    lut, status = hr_match(hist_s, target)
+    out = hr_apply(x, lut)
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import HrError
+
+__all__ = ["Params", "HrError", "hr_histogram", "hr_solve", "hr_match", "hr_apply", "hr_enhance",
+           "hr_enhance_debug", "workspace_bytes", "version", "profile_enable", "profile_collect"]
+
+
+@dataclass
+class Params:
+    """Algorithm 1 + reprocessing parameters (hr_params; readings R7, R11-R14)."""
+
+    levels: int = 256
+    max_iter: int = 10
+    alpha: float = 0.1
+    beta: float = 1e-3
+    gamma: float = 2.2
+    epsilon: float = 1e-3  # relative to N^2
+    use_epsilon: int = 0
+    update_form: int = 0  # 0 gradient-consistent, 1 paper-literal
+    grad_norm: int = 0  # 0 MAXNORM, 1 RAW_CLAMP
+
+    def c(self) -> _lib.HrParams:
+        return _lib.HrParams(self.levels, self.max_iter, self.alpha, self.beta, self.gamma,
+                             self.epsilon, self.use_epsilon, self.update_form, self.grad_norm, 0)
+
+
+_ctx: dict[int, ctypes.c_void_p] = {}
+
+
+def _context(device: torch.device) -> ctypes.c_void_p:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    c = _ctx.get(idx)
+    if c is None:
+        lib = _lib.load()
+        c = ctypes.c_void_p()
+        st = lib.hr_create(ctypes.byref(c), idx)
+        if st != 0:
+            raise HrError(st, f"hr_create(device={idx}) failed: {lib.hr_status_string(st).decode()}")
+        _ctx[idx] = c
+    return c
+
+
+def _check(st: int, ctx) -> None:
+    if st != 0:
+        lib = _lib.load()
+        raise HrError(st, f"{lib.hr_status_string(st).decode()}: {lib.hr_last_error(ctx).decode()}")
+
+
+def _cuda(t: torch.Tensor, dtype: torch.dtype, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _images(x: torch.Tensor):
+    _cuda(x, torch.uint8, "rgb")
+    if x.dim() == 3:
+        x = x.unsqueeze(0)
+    if x.dim() != 4 or x.shape[-1] != 3:
+        raise ValueError("rgb must be uint8 [B, H, W, 3] or [H, W, 3]")
+    return x
+
+
+def workspace_bytes(B: int, H: int, W: int) -> int:
+    return int(_lib.load().hr_workspace_bytes(B, H, W))
+
+
+def _workspace(B, H, W, device) -> torch.Tensor:
+    return torch.empty(max(workspace_bytes(B, H, W), 256), dtype=torch.uint8, device=device)
+
+
+def version() -> str:
+    return _lib.load().hr_version().decode()
+
+
+def hr_histogram(rgb: torch.Tensor, grad_norm: int = 0):
+    """(1) value-channel and gradient histograms.  Returns (hist_s[B,256], hist_g[B,256],
+    hist_g_raw[B,512]) as int32 tensors holding uint32 counts."""
+    x = _images(rgb)
+    B, H, W, _ = x.shape
+    dev = x.device
+    hs = torch.empty((B, 256), dtype=torch.int32, device=dev)
+    hg = torch.empty((B, 256), dtype=torch.int32, device=dev)
+    hgr = torch.empty((B, 512), dtype=torch.int32, device=dev)
+    ws = _workspace(B, H, W, dev)
+    ctx = _context(dev)
+    _check(_lib.load().hr_histogram(ctx, _ptr(x), B, H, W, grad_norm, _ptr(hs), _ptr(hg), _ptr(hgr),
+                                    _ptr(ws), _stream(dev)), ctx)
+    return hs, hg, hgr
+
+
+def hr_solve(hist_s: torch.Tensor, hist_g: torch.Tensor, params: Params | None = None):
+    """(2) Algorithm 1 + Eqs. 17-20.  Returns (hL, hR, target) float64 [B,256] and iters int32 [B]."""
+    p = params or Params()
+    _cuda(hist_s, torch.int32, "hist_s")
+    _cuda(hist_g, torch.int32, "hist_g")
+    B = hist_s.shape[0]
+    dev = hist_s.device
+    hL = torch.empty((B, 256), dtype=torch.float64, device=dev)
+    hR = torch.empty_like(hL)
+    tg = torch.empty_like(hL)
+    it = torch.empty((B,), dtype=torch.int32, device=dev)
+    pc = p.c()
+    ws = _workspace(B, 1, 1, dev)
+    ctx = _context(dev)
+    _check(_lib.load().hr_solve(ctx, _ptr(hist_s), _ptr(hist_g), B, ctypes.byref(pc), _ptr(hL), _ptr(hR),
+                                _ptr(tg), _ptr(it), _ptr(ws), _stream(dev)), ctx)
+    return hL, hR, tg, it
+
+
+def hr_match(hist_s: torch.Tensor, target: torch.Tensor):
+    """(3) CDF + LUT.  Returns (lut uint8 [B,256], status int32 [B])."""
+    _cuda(hist_s, torch.int32, "hist_s")
+    _cuda(target, torch.float64, "target")
+    B = hist_s.shape[0]
+    dev = hist_s.device
+    lut = torch.empty((B, 256), dtype=torch.uint8, device=dev)
+    stt = torch.empty((B,), dtype=torch.int32, device=dev)
+    ctx = _context(dev)
+    _check(_lib.load().hr_match(ctx, _ptr(hist_s), _ptr(target), B, _ptr(lut), _ptr(stt), _stream(dev)), ctx)
+    return lut, stt
+
+
+def hr_apply(rgb: torch.Tensor, lut: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """(4) per-pixel LUT + colour reconstruction."""
+    x = _images(rgb)
+    B, H, W, _ = x.shape
+    _cuda(lut, torch.uint8, "lut")
+    if out is None:
+        out = torch.empty_like(x)
+    ctx = _context(x.device)
+    _check(_lib.load().hr_apply(ctx, _ptr(x), _ptr(lut), B, H, W, _ptr(out), _stream(x.device)), ctx)
+    return out
+
+
+def hr_enhance(rgb: torch.Tensor, params: Params | None = None, out: torch.Tensor | None = None,
+               workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """(1)-(4) for the whole batch."""
+    p = params or Params()
+    x = _images(rgb)
+    B, H, W, _ = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    ws = workspace if workspace is not None else _workspace(B, H, W, x.device)
+    pc = p.c()
+    ctx = _context(x.device)
+    _check(_lib.load().hr_enhance(ctx, _ptr(x), B, H, W, ctypes.byref(pc), _ptr(out), _ptr(ws),
+                                  _stream(x.device)), ctx)
+    return out
+
+
+def profile_enable(device=None, on: bool = True) -> None:
+    """Record per-stage CUDA events inside every hr_enhance on `device` (measurement only)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    ctx = _context(dev)
+    _check(_lib.load().hr_profile_enable(ctx, 1 if on else 0), ctx)
+
+
+def profile_collect(device=None):
+    """Summed (hist_ms, solve_ms, apply_ms) and the number of hr_enhance calls since the last
+    collect (waits for the recorded events)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    ctx = _context(dev)
+    ms = (ctypes.c_double * 3)()
+    n = ctypes.c_int32(0)
+    _check(_lib.load().hr_profile_collect(ctx, ms, ctypes.byref(n)), ctx)
+    return (ms[0], ms[1], ms[2]), n.value
+
+
+def hr_enhance_debug(rgb: torch.Tensor, params: Params | None = None):
+    """hr_enhance also returning the intermediate hist_s, lut and iteration counts."""
+    p = params or Params()
+    x = _images(rgb)
+    B, H, W, _ = x.shape
+    dev = x.device
+    out = torch.empty_like(x)
+    hs = torch.empty((B, 256), dtype=torch.int32, device=dev)
+    lut = torch.empty((B, 256), dtype=torch.uint8, device=dev)
+    it = torch.empty((B,), dtype=torch.int32, device=dev)
+    ws = _workspace(B, H, W, dev)
+    pc = p.c()
+    ctx = _context(dev)
+    _check(_lib.load().hr_enhance_debug(ctx, _ptr(x), B, H, W, ctypes.byref(pc), _ptr(out), _ptr(ws),
+                                        _ptr(hs), _ptr(lut), _ptr(it), _stream(dev)), ctx)
+    return out, hs, lut, it

@@ -1,0 +1,313 @@
+// hr_api.cu -- the C-ABI boundary (include/histretinex.h): validation, context, launches.
+//
+// Every entry point validates synchronously and enqueues nothing on error.  No exception
+// or exit() crosses the boundary.
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+#include <vector>
+
+#include "hr_common.cuh"
+
+struct hr_ctx {
+  int device = 0;
+  int num_sms = 148;
+  int l2_bytes = 0;
+  char last_error[512] = {0};
+  // stage timing (hr_profile_*)
+  bool prof = false;
+  int prof_used = 0;
+  std::vector<cudaEvent_t> prof_ev;  // 4 per recorded call
+};
+
+namespace {
+
+using hr::kGradSlots;
+using hr::kLevels;
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct WsLayout {
+  size_t hist_s, graw, lut, iters, total;
+};
+
+WsLayout ws_layout(int64_t B) {
+  WsLayout L;
+  size_t o = 0;
+  L.hist_s = o;
+  o = align_up(o + (size_t)B * kLevels * sizeof(uint32_t));
+  L.graw = o;
+  o = align_up(o + (size_t)B * kGradSlots * sizeof(uint32_t));
+  L.lut = o;
+  o = align_up(o + (size_t)B * kLevels);
+  L.iters = o;
+  o = align_up(o + (size_t)B * sizeof(int32_t));
+  L.total = o;
+  return L;
+}
+
+hr_status set_err(hr_ctx* c, hr_status s, const char* msg) {
+  if (c) snprintf(c->last_error, sizeof c->last_error, "%s", msg);
+  return s;
+}
+
+hr_status cuda_err(hr_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return HR_OK;
+  if (c) snprintf(c->last_error, sizeof c->last_error, "%s: %s", where, cudaGetErrorString(e));
+  return HR_ECUDA;
+}
+
+hr_status check_shape(hr_ctx* c, int64_t B, int32_t H, int32_t W) {
+  if (B < 1 || H < 0 || W < 0) return set_err(c, HR_EINVAL, "B must be >= 1 and H, W >= 0");
+  if ((int64_t)H * W == 0) return set_err(c, HR_EEMPTY, "empty image (H*W == 0)");
+  if (B > (1 << 30) || (int64_t)H * W > (int64_t)1 << 32) return set_err(c, HR_EINVAL, "size too large");
+  return HR_OK;
+}
+
+hr_status check_params(hr_ctx* c, const hr_params* p) {
+  if (!p) return set_err(c, HR_EINVAL, "params is NULL");
+  if (p->levels != 256) return set_err(c, HR_EUNSUPPORTED, "levels must be 256");
+  if (!(p->alpha > 0) || !(p->beta > 0)) return set_err(c, HR_EINVAL, "alpha and beta must be > 0");
+  if (!(p->gamma >= 1.0)) return set_err(c, HR_EINVAL, "gamma must be >= 1");
+  if (!(p->epsilon > 0)) return set_err(c, HR_EINVAL, "epsilon must be > 0");
+  if (p->max_iter < 1) return set_err(c, HR_EINVAL, "max_iter must be >= 1");
+  if (p->use_epsilon != 0 && p->use_epsilon != 1) return set_err(c, HR_EINVAL, "use_epsilon must be 0/1");
+  if (p->update_form != 0 && p->update_form != 1) return set_err(c, HR_EINVAL, "update_form must be 0/1");
+  if (p->grad_norm != 0 && p->grad_norm != 1) return set_err(c, HR_EINVAL, "grad_norm must be 0/1");
+  if (p->reserved != 0) return set_err(c, HR_EINVAL, "reserved must be 0");
+  return HR_OK;
+}
+
+hr_status activate(hr_ctx* c) {
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_err(c, e, "cudaGetDevice");
+  if (cur != c->device) {
+    e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return cuda_err(c, e, "cudaSetDevice");
+  }
+  return HR_OK;
+}
+
+int hist_grid(const hr_ctx* c) { return 2 * c->num_sms; }
+int apply_grid(const hr_ctx* c) { return 8 * c->num_sms; }
+
+}  // namespace
+
+extern "C" {
+
+hr_status hr_default_params(hr_params* p) {
+  if (!p) return HR_EINVAL;
+  p->levels = 256;
+  p->max_iter = 10;
+  p->alpha = 0.1;
+  p->beta = 1e-3;
+  p->gamma = 2.2;
+  p->epsilon = 1e-3;
+  p->use_epsilon = 0;
+  p->update_form = 0;
+  p->grad_norm = 0;
+  p->reserved = 0;
+  return HR_OK;
+}
+
+hr_status hr_create(hr_ctx** out, int device) {
+  if (!out) return HR_EINVAL;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+    cudaGetLastError();
+    return HR_ECUDA;
+  }
+  hr_ctx* c = new (std::nothrow) hr_ctx();
+  if (!c) return HR_ECUDA;
+  c->device = device;
+  if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&c->l2_bytes, cudaDevAttrL2CacheSize, device) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return HR_ECUDA;
+  }
+  *out = c;
+  return HR_OK;
+}
+
+hr_status hr_destroy(hr_ctx* c) {
+  if (c) {
+    for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  }
+  delete c;
+  return HR_OK;
+}
+
+hr_status hr_profile_enable(hr_ctx* c, int32_t on) {
+  if (!c) return HR_EINVAL;
+  c->prof = on != 0;
+  c->prof_used = 0;
+  return HR_OK;
+}
+
+hr_status hr_profile_collect(hr_ctx* c, double* stage_ms, int32_t* steps) {
+  if (!c || !stage_ms) return HR_EINVAL;
+  hr_status s = activate(c);
+  if (s) return s;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int i = 0; i < c->prof_used; ++i) {
+    cudaEvent_t* e = &c->prof_ev[4 * i];
+    cudaError_t err = cudaEventSynchronize(e[3]);
+    if (err != cudaSuccess) return cuda_err(c, err, "hr_profile_collect");
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      err = cudaEventElapsedTime(&ms, e[k], e[k + 1]);
+      if (err != cudaSuccess) return cuda_err(c, err, "hr_profile_collect");
+      acc[k] += ms;
+    }
+  }
+  for (int k = 0; k < 3; ++k) stage_ms[k] = acc[k];
+  if (steps) *steps = c->prof_used;
+  c->prof_used = 0;
+  return HR_OK;
+}
+
+const char* hr_status_string(hr_status s) {
+  switch (s) {
+    case HR_OK: return "ok";
+    case HR_EINVAL: return "invalid argument";
+    case HR_EEMPTY: return "empty input";
+    case HR_EDEGENERATE: return "degenerate histogram";
+    case HR_ECUDA: return "CUDA error";
+    case HR_EUNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* hr_last_error(const hr_ctx* c) { return c ? c->last_error : ""; }
+
+const char* hr_version(void) { return "histretinex-b200 0.1 sm_100a"; }
+
+size_t hr_workspace_bytes(int64_t B, int32_t H, int32_t W) {
+  if (B < 1 || H < 0 || W < 0) return 0;
+  (void)H;
+  (void)W;
+  return ws_layout(B).total;
+}
+
+hr_status hr_histogram(hr_ctx* c, const uint8_t* rgb, int64_t B, int32_t H, int32_t W, int32_t grad_norm,
+                       uint32_t* hist_s, uint32_t* hist_g, uint32_t* hist_g_raw, void* ws, void* stream) {
+  if (!c) return HR_EINVAL;
+  hr_status s = check_shape(c, B, H, W);
+  if (s) return s;
+  if (!rgb || !hist_s || !hist_g || !ws) return set_err(c, HR_EINVAL, "NULL pointer");
+  if (grad_norm != 0 && grad_norm != 1) return set_err(c, HR_EINVAL, "grad_norm must be 0/1");
+  if ((s = activate(c))) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const WsLayout L = ws_layout(B);
+  uint32_t* graw = hist_g_raw ? hist_g_raw : reinterpret_cast<uint32_t*>((char*)ws + L.graw);
+  cudaError_t e = cudaMemsetAsync(hist_s, 0, (size_t)B * kLevels * sizeof(uint32_t), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(graw, 0, (size_t)B * kGradSlots * sizeof(uint32_t), st);
+  if (e == cudaSuccess) e = hr::launch_hist(rgb, B, H, W, hist_s, graw, hist_grid(c), st);
+  if (e == cudaSuccess) e = hr::launch_remap(graw, B, grad_norm, hist_g, st);
+  return cuda_err(c, e, "hr_histogram");
+}
+
+hr_status hr_solve(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, int64_t B, const hr_params* p,
+                   double* hL, double* hR, double* target, int32_t* iters, void* ws, void* stream) {
+  if (!c) return HR_EINVAL;
+  if (!hist_s || !hist_g || !hL || !hR || !target) return set_err(c, HR_EINVAL, "NULL pointer");
+  if (B < 1 || B > (1 << 30)) return set_err(c, HR_EINVAL, "B must be >= 1");
+  hr_status s = check_params(c, p);
+  if (s) return s;
+  if ((s = activate(c))) return s;
+  (void)ws;
+  hr::SolveArgs a{};
+  a.hist_s = hist_s;
+  a.hist_g = hist_g;
+  a.graw = nullptr;
+  a.grad_norm = p->grad_norm;
+  a.p = *p;
+  a.hL = hL;
+  a.hR = hR;
+  a.target = target;
+  a.iters = iters;
+  a.lut = nullptr;
+  a.status = nullptr;
+  return cuda_err(c, hr::launch_solve(a, B, (cudaStream_t)stream), "hr_solve");
+}
+
+hr_status hr_match(hr_ctx* c, const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,
+                   int32_t* img_status, void* stream) {
+  if (!c) return HR_EINVAL;
+  if (!hist_s || !target || !lut) return set_err(c, HR_EINVAL, "NULL pointer");
+  if (B < 1 || B > (1 << 30)) return set_err(c, HR_EINVAL, "B must be >= 1");
+  hr_status s = activate(c);
+  if (s) return s;
+  return cuda_err(c, hr::launch_match(hist_s, target, B, lut, img_status, (cudaStream_t)stream), "hr_match");
+}
+
+hr_status hr_apply(hr_ctx* c, const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
+                   void* stream) {
+  if (!c) return HR_EINVAL;
+  hr_status s = check_shape(c, B, H, W);
+  if (s) return s;
+  if (!in || !lut || !out) return set_err(c, HR_EINVAL, "NULL pointer");
+  if ((s = activate(c))) return s;
+  return cuda_err(c, hr::launch_apply(in, lut, B, H, W, out, apply_grid(c), (cudaStream_t)stream), "hr_apply");
+}
+
+hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, const hr_params* p,
+                           uint8_t* out, void* ws, uint32_t* hist_s_dbg, uint8_t* lut_dbg, int32_t* iters_dbg,
+                           void* stream) {
+  if (!c) return HR_EINVAL;
+  hr_status s = check_shape(c, B, H, W);
+  if (s) return s;
+  if ((s = check_params(c, p))) return s;
+  if (!in || !out || !ws) return set_err(c, HR_EINVAL, "NULL pointer");
+  if (in == out) return set_err(c, HR_EINVAL, "rgb_out must not alias rgb_in");
+  if ((s = activate(c))) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t* ev = nullptr;
+  if (c->prof) {
+    if (c->prof_used >= 4096) return set_err(c, HR_EINVAL, "profile buffer full: call hr_profile_collect");
+    while ((int)c->prof_ev.size() < 4 * (c->prof_used + 1)) {
+      cudaEvent_t e;
+      cudaError_t err = cudaEventCreate(&e);
+      if (err != cudaSuccess) return cuda_err(c, err, "cudaEventCreate");
+      c->prof_ev.push_back(e);
+    }
+    ev = &c->prof_ev[4 * c->prof_used];
+    c->prof_used++;
+  }
+  auto mark = [&](int k) -> cudaError_t { return ev ? cudaEventRecord(ev[k], st) : cudaSuccess; };
+  const WsLayout L = ws_layout(B);
+  uint32_t* hs = hist_s_dbg ? hist_s_dbg : reinterpret_cast<uint32_t*>((char*)ws + L.hist_s);
+  uint32_t* graw = reinterpret_cast<uint32_t*>((char*)ws + L.graw);
+  uint8_t* lut = lut_dbg ? lut_dbg : reinterpret_cast<uint8_t*>((char*)ws + L.lut);
+  cudaError_t e = mark(0);
+  if (e == cudaSuccess) e = cudaMemsetAsync(hs, 0, (size_t)B * kLevels * sizeof(uint32_t), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(graw, 0, (size_t)B * kGradSlots * sizeof(uint32_t), st);
+  if (e == cudaSuccess) e = hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st);
+  if (e == cudaSuccess) e = mark(1);
+  if (e == cudaSuccess) {
+    hr::SolveArgs a{};
+    a.hist_s = hs;
+    a.hist_g = nullptr;
+    a.graw = graw;
+    a.grad_norm = p->grad_norm;
+    a.p = *p;
+    a.iters = iters_dbg;
+    a.lut = lut;
+    e = hr::launch_solve(a, B, st);
+  }
+  if (e == cudaSuccess) e = mark(2);
+  if (e == cudaSuccess) e = hr::launch_apply(in, lut, B, H, W, out, apply_grid(c), st);
+  if (e == cudaSuccess) e = mark(3);
+  return cuda_err(c, e, "hr_enhance");
+}
+
+hr_status hr_enhance(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, const hr_params* p,
+                     uint8_t* out, void* ws, void* stream) {
+  return hr_enhance_debug(c, in, B, H, W, p, out, ws, nullptr, nullptr, nullptr, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// hr_common.cuh -- shared device-side definitions of the HistRetinex CUDA path (sm_100a).
+//
+// Product code.  Shares nothing with oracle/ (the CPU test oracle).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/histretinex.h"
+
+namespace hr {
+
+constexpr int kLevels = 256;     // l (the only level count of this build)
+constexpr int kGradSlots = 512;  // raw gradient |dx|+|dy| in [0, 510]
+constexpr int kMaxGrad = 510;
+
+// ---------------------------------------------------------------- k_hist
+constexpr int kHistThreads = 512;  // 16 warps; 2 CTAs per SM (96 KB smem each)
+constexpr int kLanes = 32;
+// Lane-private sub-histograms: counter for bin v of lane l at word v*32 + l, so every
+// smem atomic of a warp hits 32 distinct banks whatever the data skew.
+constexpr int kHistSmemBytes = (kLevels + kGradSlots) * kLanes * 4;  // 98,304 B
+
+// ---------------------------------------------------------------- k_solve
+constexpr int kSolveThreads = 256;  // one thread per level for the per-bin phases
+constexpr int kSolveWarps = kSolveThreads / 32;
+
+// ---------------------------------------------------------------- k_apply
+constexpr int kApplyThreads = 256;
+
+// Launch helpers implemented in the kernel translation units.
+cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
+                        uint32_t* hist_graw, int grid, cudaStream_t st);
+cudaError_t launch_remap(const uint32_t* hist_graw, int64_t B, int32_t grad_norm, uint32_t* hist_g,
+                         cudaStream_t st);
+
+struct SolveArgs {
+  const uint32_t* hist_s;   // [B][256]
+  const uint32_t* hist_g;   // [B][256] remapped gradient histogram, or NULL -> use graw
+  const uint32_t* graw;     // [B][512] raw gradient histogram (used when hist_g == NULL)
+  int32_t grad_norm;        // remap mode when reading graw
+  hr_params p;
+  double* hL;               // [B][256] nullable
+  double* hR;               // [B][256] nullable
+  double* target;           // [B][256] nullable
+  int32_t* iters;           // [B] nullable
+  uint8_t* lut;             // [B][256] nullable (fused CDF + LUT tail)
+  int32_t* status;          // [B] nullable
+};
+cudaError_t launch_solve(const SolveArgs& a, int64_t B, cudaStream_t st);
+size_t solve_smem_bytes();
+
+cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,
+                         int32_t* status, cudaStream_t st);
+
+cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
+                         uint8_t* out, int grid, cudaStream_t st);
+
+}  // namespace hr

@@ -1,0 +1,667 @@
+// k_solve.cu -- kernel (b): batched histogram-domain Retinex solver (Algorithm 1) in fp64,
+// with the Eq. 17-20 reprocessing and the fused CDF + histogram-matching LUT tail (c).
+//
+// One CTA (256 threads) per image.  PAPER.md references:
+//   Eq. 6  count matrix  C_ij = hR_i hL_j / N          -- never materialised
+//   Eq. 7  location matrix b_i b_j (R1, R2)            -- constant: idx(i,j)
+//   P:192           index(i,j) = nearest bin of b_i b_j          = (i*j + 127) div 255
+//   Eq. 8  Est_k = sum_{idx(i,j)=k} C_ij (R3)
+//   Eq. 11  K_ij = C_ij / Est_idx(i,j) (R8)
+//   Eq. 13, Eq. 12, Eqs. 15, 14, Alg. 1 loop
+//   Eqs. 17-20 enhanced histogram with index_1 (R4, R5)
+//   P:308 histogram matching (R16)
+//
+// Factored form.  With rho_k = hS_k / EstRaw_k (EstRaw = N Est):
+//   Eq. 13 (gradient-consistent, R7): hR'_i = (hR_i A_i / N + beta hG_i) / (sum hL^2/N^2 + beta),
+//        A_i = sum_j hL_j^2 rho_idx(i,j)
+//   Eq. 12: hL'_j = (hL_j B_j / N + alpha hS_j) / (sum hR'^2/N^2 + alpha),
+//        B_j = sum_i hR'_i hR_i rho_idx(i,j)         (K frozen at iteration t, R10)
+//   Paper-literal form (K_ij as a divisor): A_i = sum_j sigma_k / hR_i, sigma_k = hS_k EstRaw_k,
+//        B_j = sum_i (hR'_i / hR_i) sigma_k / hL_j   (both divided by N).
+// Supports never change (hR stays 0 off supp(hG), hL off supp(hS)), so every pass runs over
+// the compacted cells sR x sL only.  All reductions are fixed-order (reduce-by-key over
+// per-thread slices + a deterministic segmented scan): results are bit-identical run to
+// run; no floating-point atomics anywhere.
+#include "hr_common.cuh"
+
+namespace hr {
+namespace {
+
+constexpr int T = kSolveThreads;
+constexpr int NW = kSolveWarps;
+constexpr int kMaxCells = kLevels * kLevels;
+
+// slots of the block-reduction scratch
+enum { R_SL2 = 0, R_SR1, R_SR2, R_SL1, R_DR, R_DL, R_N, kSlots };
+
+struct __align__(16) Sm {
+  double hR[kLevels], hL[kLevels];    // compacted state (index a over sR, c over sL)
+  double hR1[kLevels], hL1[kLevels];  // raw updates (Eq. 13 / Eq. 12 outputs)
+  double hSc[kLevels], hGc[kLevels];  // priors at the support entries
+  double wgt[kLevels];                // per-row weight of the L-pass
+  double hSd[kLevels];                // dense hS as double
+  double est[kLevels];                // EstRaw_k (= N Est_k)
+  double rho[kLevels];                // rho_k (GC) or sigma_k (paper-literal)
+  double rowsum[kLevels], colsum[kLevels];
+  double bk[kLevels];                 // b_k = k/255 (R1)
+  double red[kSlots][NW];
+  // reduce-by-key scratch
+  double sfA[T], slA[T], outA[T];
+  double wv[NW];
+  int kfA[T], klA[T];
+  int wf[NW];
+  uint8_t hasA[T];
+  // supports
+  uint32_t hSi[kLevels], hGi[kLevels];
+  int cstart[kLevels + 1];
+  uint16_t posL[kLevels + 1];
+  uint8_t listR[kLevels], listL[kLevels];
+  int nR, nL, E;
+  uint64_t Nint;
+};
+// the Eq. 20 pass and the CDF tail reuse the iteration arrays (dead by then)
+
+__device__ __forceinline__ int idx0(int i, int j) {  // P:192 index(i,j) for l = 256
+  return (int)(((uint32_t)(i * j + 127) * 32897u) >> 23);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
+// Sum over warps in fixed order (call after a barrier that follows the slot writes).
+__device__ __forceinline__ double slot_sum(const Sm& s, int slot) {
+  double a = 0.0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) a += s.red[slot][w];
+  return a;
+}
+
+__device__ __forceinline__ void slot_put(Sm& s, int slot, double v) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) s.red[slot][threadIdx.x >> 5] = v;
+}
+
+// Per-thread run accumulator for reduce-by-key over a contiguous slice whose keys are
+// non-decreasing.  Runs strictly inside the slice are owned by this thread and written
+// directly; the first and last runs may continue into neighbouring slices.
+struct Runs {
+  int cur, kf;
+  double acc, sf;
+  bool first;
+  __device__ __forceinline__ void begin(int k, double v) {
+    cur = k;
+    acc = v;
+    first = true;
+  }
+  __device__ __forceinline__ void step(int k, double v, double* out) {
+    if (k == cur) {
+      acc += v;
+    } else {
+      if (first) {
+        kf = cur;
+        sf = acc;
+        first = false;
+      } else {
+        out[cur] = acc;
+      }
+      cur = k;
+      acc = v;
+    }
+  }
+};
+
+// Deterministic combination of the per-thread boundary runs (segmented scan over threads).
+// On return (after the trailing barrier) out[key] holds the full sum of every key that
+// occurs in the slices.
+__device__ void rbk_combine(Sm& s, bool has, const Runs& r, double* out) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const bool single = has && r.first;
+  const int kf = has ? (single ? r.cur : r.kf) : -1;
+  const double sf = has ? (single ? r.acc : r.sf) : 0.0;
+  const int kl = has ? r.cur : -2;
+  const double sl = has ? r.acc : 0.0;
+  s.kfA[tid] = kf;
+  s.klA[tid] = kl;
+  s.hasA[tid] = has;
+  __syncthreads();
+  const bool prevHas = tid > 0 && s.hasA[tid - 1];
+  const bool prevSame = prevHas && s.klA[tid - 1] == kf;
+  bool f = !(has && single && prevSame);  // head of a chain of single-key slices
+  double v = sl;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double vu = __shfl_up_sync(0xffffffffu, v, d);
+    const bool fu = __shfl_up_sync(0xffffffffu, (int)f, d) != 0;
+    if (lane >= d) {
+      if (!f) v = vu + v;
+      f = f || fu;
+    }
+  }
+  if (lane == 31) {
+    s.wv[w] = v;
+    s.wf[w] = f;
+  }
+  __syncthreads();
+  if (!f) {
+    double cv = 0.0;
+    for (int u = 0; u < w; ++u) cv = s.wf[u] ? s.wv[u] : cv + s.wv[u];
+    v = cv + v;
+  }
+  s.outA[tid] = v;
+  __syncthreads();
+  if (has) {
+    if (!single) out[kf] = sf + (prevSame ? s.outA[tid - 1] : 0.0);
+    const bool nextCont = tid + 1 < T && s.hasA[tid + 1] && s.kfA[tid + 1] == kl;
+    if (!nextCont) out[kl] = v;
+  }
+  __syncthreads();
+}
+
+// inclusive block scan of non-negative ints (exact)
+__device__ int block_scan_excl(int x, int* total, int* wscratch) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int v = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += u;
+  }
+  if (lane == 31) wscratch[w] = v;
+  __syncthreads();
+  int off = 0, tot = 0;
+  for (int u = 0; u < NW; ++u) {
+    if (u < w) off += wscratch[u];
+    tot += wscratch[u];
+  }
+  __syncthreads();
+  *total = tot;
+  return off + v - x;
+}
+
+// c-range [lo, hi] of the compacted columns whose index(i, j) == k (idx monotone in j)
+__device__ __forceinline__ void crange(const Sm& s, int i, int k, int& lo, int& hi) {
+  if (i == 0) {  // index(0, j) = 0 for all j
+    lo = 0;
+    hi = (k == 0) ? s.nL - 1 : -1;
+    return;
+  }
+  // (i*j + 127) div 255 == k  <=>  255k - 127 <= i*j <= 255k + 127
+  const int a = 255 * k - 127, bnd = 255 * k + 127;
+  int jlo = a <= 0 ? 0 : (a + i - 1) / i;
+  int jhi = bnd / i;
+  if (jhi > 255) jhi = 255;
+  if (jlo > jhi) {
+    lo = 0;
+    hi = -1;
+    return;
+  }
+  lo = s.posL[jlo];
+  hi = (int)s.posL[jhi + 1] - 1;
+}
+
+// index_1(i,j) of Eqs. 17-19: first k minimising |b_i p_j - b_k|, p_j = b_j^(1/gamma).
+__device__ __forceinline__ int idx1(const Sm& s, double bi, double pj) {
+  const double x = __dmul_rn(bi, pj);  // rounded product (no contraction into the compare)
+  int k0 = (int)floor(x * 255.0);
+  int best = -1;
+  double bd = 0.0;
+#pragma unroll
+  for (int d = -1; d <= 1; ++d) {
+    const int k = k0 + d;
+    if (k < 0 || k > 255) continue;
+    const double dist = fabs(x - s.bk[k]);
+    if (best < 0 || dist < bd) {
+      bd = dist;
+      best = k;
+    }
+  }
+  return best;
+}
+
+// CDF + LUT (R16), shared by the solver tail and k_match.  T: dense target [256] in
+// smem, hSi: dense counts in smem.  Uses Pt/Ct/Cs scratch (3 x 256 doubles).
+__device__ void cdf_lut(const uint32_t* hSi, const double* Tt, double* Pt, double* Ct, double* Cs,
+                        int* wscr, uint8_t* lut_out, int32_t* status_out) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  // integer prefix of hS (exact in any order)
+  unsigned long long v = hSi[tid];
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long u = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += u;
+  }
+  __shared__ unsigned long long wtot[NW];
+  if (lane == 31) wtot[tid >> 5] = v;
+  __syncthreads();
+  unsigned long long off = 0, Ntot = 0;
+  for (int u = 0; u < NW; ++u) {
+    if (u < (tid >> 5)) off += wtot[u];
+    Ntot += wtot[u];
+  }
+  const unsigned long long Ps = off + v;
+  Cs[tid] = Ntot ? (double)Ps / (double)Ntot : 0.0;
+  // plateau-preserving prefix of the target: lane-sequential blocks of 8, sequential carry
+  if (tid < 32) {
+    double loc[8];
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      acc = (m == 0) ? Tt[8 * tid] : acc + Tt[8 * tid + m];
+      loc[m] = acc;
+    }
+    // carry_l = carry_{l-1} + total_{l-1}, strictly sequential over lanes
+    double carry = 0.0;
+    for (int l = 0; l < 32; ++l) {
+      const double tot = __shfl_sync(0xffffffffu, acc, l);
+      if (l < tid) carry = carry + tot;  // carry for lane tid: sum in lane order
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) Pt[8 * tid + m] = (tid == 0) ? loc[m] : carry + loc[m];
+  }
+  __syncthreads();
+  const double last = Pt[kLevels - 1];
+  const bool degenerate = !(last > 0.0) || Ntot == 0;
+  Ct[tid] = degenerate ? 0.0 : Pt[tid] / last;
+  __syncthreads();
+  int res = tid;
+  if (!degenerate) {
+    const double x = Cs[tid];
+    // k* = first k with Ct[k] >= x
+    int lo = 0, hi = kLevels;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (Ct[mid] >= x) hi = mid; else lo = mid + 1;
+    }
+    const int ks = lo;  // <= 255 because Ct[255] == 1 >= x
+    res = ks;
+    if (ks > 0) {
+      const double cprev = Ct[ks - 1];
+      // first index of the plateau holding Ct[ks-1]
+      int l2 = 0, h2 = ks - 1;
+      while (l2 < h2) {
+        const int mid = (l2 + h2) >> 1;
+        if (Ct[mid] >= cprev) h2 = mid; else l2 = mid + 1;
+      }
+      const double d0 = fabs(cprev - x);
+      const double d1 = fabs(Ct[ks] - x);
+      if (d0 <= d1) res = l2;  // ties -> smallest k
+    }
+  }
+  if (lut_out) lut_out[tid] = (uint8_t)res;
+  if (status_out && tid == 0) *status_out = degenerate ? (int32_t)HR_EDEGENERATE : (int32_t)HR_OK;
+  (void)wscr;
+}
+
+__device__ void remap_gradient(const uint32_t* graw, int grad_norm, uint32_t* hGi, int* wscr) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t c0 = graw[tid], c1 = graw[tid + T];
+  int m = c1 ? tid + T : (c0 ? tid : 0);
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
+  if (lane == 0) wscr[tid >> 5] = m;
+  hGi[tid] = 0u;
+  __syncthreads();
+  int gmax = 0;
+  for (int u = 0; u < NW; ++u) gmax = max(gmax, wscr[u]);
+  auto level = [&](int g) -> int {
+    if (grad_norm == 1) return g < 255 ? g : 255;                         // RAW_CLAMP
+    return gmax == 0 ? 0 : (int)((510u * (uint32_t)g + (uint32_t)gmax) / (2u * (uint32_t)gmax));  // MAXNORM
+  };
+  if (c0) atomicAdd(&hGi[level(tid)], c0);
+  if (c1) atomicAdd(&hGi[level(tid + T)], c1);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Sm& s = *reinterpret_cast<Sm*>(smraw);
+  uint16_t* cells = reinterpret_cast<uint16_t*>(smraw + sizeof(Sm));
+  __shared__ int wscr[NW];
+  const int tid = threadIdx.x;
+  const int64_t b = blockIdx.x;
+  const hr_params& P = args.p;
+
+  // ---- histograms (Alg. 1 init) ----
+  s.hSi[tid] = args.hist_s[b * kLevels + tid];
+  if (args.hist_g) {
+    s.hGi[tid] = args.hist_g[b * kLevels + tid];
+  } else {
+    remap_gradient(args.graw + b * kGradSlots, args.grad_norm, s.hGi, wscr);
+  }
+  s.bk[tid] = (double)tid / 255.0;
+  s.hSd[tid] = (double)s.hSi[tid];
+  __syncthreads();
+
+  // ---- supports (fixed for all t) ----
+  const bool fL = s.hSi[tid] != 0u, fR = s.hGi[tid] != 0u;
+  int nL, nR;
+  const int pL = block_scan_excl(fL ? 1 : 0, &nL, wscr);
+  const int pR = block_scan_excl(fR ? 1 : 0, &nR, wscr);
+  if (fL) s.listL[pL] = (uint8_t)tid;
+  if (fR) s.listR[pR] = (uint8_t)tid;
+  s.posL[tid] = (uint16_t)pL;
+  if (tid == 0) {
+    s.posL[kLevels] = (uint16_t)nL;
+    s.nL = nL;
+    s.nR = nR;
+  }
+  // N = sum hS (exact integer)
+  {
+    unsigned long long v = s.hSi[tid];
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    __shared__ unsigned long long nw[NW];
+    if ((tid & 31) == 0) nw[tid >> 5] = v;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long n = 0;
+      for (int u = 0; u < NW; ++u) n += nw[u];
+      s.Nint = n;
+    }
+  }
+  __syncthreads();
+  const double N = (double)s.Nint;
+  if (s.Nint == 0 || nR == 0) {  // empty image: zero outputs (never for validated inputs)
+    if (args.hL) args.hL[b * kLevels + tid] = 0.0;
+    if (args.hR) args.hR[b * kLevels + tid] = 0.0;
+    if (args.target) args.target[b * kLevels + tid] = 0.0;
+    if (args.lut) args.lut[b * kLevels + tid] = (uint8_t)tid;
+    if (tid == 0) {
+      if (args.iters) args.iters[b] = 0;
+      if (args.status) args.status[b] = HR_EDEGENERATE;
+    }
+    return;
+  }
+
+  // ---- compacted state: hR^0 = hG, hL^0 = hS (R9) ----
+  if (tid < nL) {
+    const double v = s.hSd[s.listL[tid]];
+    s.hL[tid] = v;
+    s.hSc[tid] = v;
+  }
+  if (tid < nR) {
+    const double v = (double)s.hGi[s.listR[tid]];
+    s.hR[tid] = v;
+    s.hGc[tid] = v;
+  }
+  s.est[tid] = 0.0;
+
+  // ---- cells sorted by output bin k = index(i,j): one thread per k ----
+  {
+    const int k = tid;
+    int cnt = 0;
+    for (int a = 0; a < nR; ++a) {
+      int lo, hi;
+      crange(s, s.listR[a], k, lo, hi);
+      if (hi >= lo) cnt += hi - lo + 1;
+    }
+    int E;
+    const int start = block_scan_excl(cnt, &E, wscr);
+    s.cstart[k] = start;
+    if (tid == 0) {
+      s.cstart[kLevels] = E;
+      s.E = E;
+    }
+    int pos = start;
+    for (int a = 0; a < nR; ++a) {
+      int lo, hi;
+      crange(s, s.listR[a], k, lo, hi);
+      for (int c = lo; c <= hi; ++c) cells[pos++] = (uint16_t)((a << 8) | c);
+    }
+  }
+  {
+    double v = tid < nL ? s.hL[tid] * s.hL[tid] : 0.0;
+    slot_put(s, R_SL2, v);
+  }
+  __syncthreads();
+
+  const int E = s.E;
+  const int ER = nR * nL;  // == E (every cell of sR x sL has exactly one k)
+  const double N2 = N * N;
+  const int form = P.update_form;
+  // E-pass slice and its first key (fixed for all iterations)
+  const int SE = (E + T - 1) / T;
+  const int e0 = min(E, tid * SE), e1 = min(E, e0 + SE);
+  int kstart = 0;
+  if (e0 < e1) {
+    int lo = 0, hi = kLevels + 1;  // upper_bound(cstart, e0) - 1
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s.cstart[mid] <= e0) lo = mid + 1; else hi = mid;
+    }
+    kstart = lo - 1;
+  }
+  const int SRW = (ER + T - 1) / T;
+  const int r0 = min(ER, tid * SRW), r1 = min(ER, r0 + SRW);
+
+  double SL2 = slot_sum(s, R_SL2);
+  int t = 0;
+  for (;;) {
+    // ---- E-pass: EstRaw_k = sum_{idx=k} hR_a hL_c  (Eq. 6 + Eq. 8 with N folded) ----
+    {
+      Runs run;
+      const bool has = e0 < e1;
+      if (has) {
+        int k = kstart;
+        for (int e = e0; e < e1; ++e) {
+          while (e >= s.cstart[k + 1]) ++k;
+          const uint32_t cl = cells[e];
+          const double v = s.hR[cl >> 8] * s.hL[cl & 255];
+          if (e == e0) run.begin(k, v); else run.step(k, v, s.est);
+        }
+      }
+      rbk_combine(s, has, run, s.est);
+    }
+    // ---- rho_k (Eq. 11 folded): GC rho = hS/EstRaw ; paper-literal sigma = hS*EstRaw ----
+    {
+      const double e = s.est[tid];
+      s.rho[tid] = form == 0 ? (e > 0.0 ? s.hSd[tid] / e : 0.0) : s.hSd[tid] * e;
+    }
+    __syncthreads();
+    // ---- R-pass: A_a over row-major cells (Eq. 13) ----
+    {
+      Runs run;
+      const bool has = r0 < r1;
+      if (has) {
+        int a = r0 / nL, c = r0 - a * nL;
+        int ia = s.listR[a];
+        for (int e = r0; e < r1; ++e) {
+          const int k = idx0(ia, s.listL[c]);
+          const double v = form == 0 ? s.hL[c] * s.hL[c] * s.rho[k] : s.rho[k];
+          if (e == r0) run.begin(a, v); else run.step(a, v, s.rowsum);
+          if (++c == nL) {
+            c = 0;
+            ++a;
+            if (a < nR) ia = s.listR[a];
+          }
+        }
+      }
+      rbk_combine(s, has, run, s.rowsum);
+    }
+    // ---- Eq. 13 finalisation per row ----
+    {
+      double v = 0.0;
+      if (tid < nR) {
+        const double hr = s.hR[tid];
+        const double num = form == 0 ? hr * s.rowsum[tid] / N : s.rowsum[tid] / (N * hr);
+        v = (num + P.beta * s.hGc[tid]) / (SL2 / N2 + P.beta);
+        v = v > 0.0 ? v : 0.0;
+        s.hR1[tid] = v;
+        s.wgt[tid] = form == 0 ? v * hr : v / hr;
+      }
+      slot_put(s, R_SR1, v);
+      slot_put(s, R_SR2, v * v);
+    }
+    __syncthreads();
+    const double SR2 = slot_sum(s, R_SR2);
+    // ---- L-pass: B_c over column-major cells (Eq. 12, frozen K) ----
+    {
+      Runs run;
+      const bool has = r0 < r1;
+      if (has) {
+        int c = r0 / nR, a = r0 - c * nR;
+        int jc = s.listL[c];
+        for (int e = r0; e < r1; ++e) {
+          const int k = idx0(s.listR[a], jc);
+          const double v = s.wgt[a] * s.rho[k];
+          if (e == r0) run.begin(c, v); else run.step(c, v, s.colsum);
+          if (++a == nR) {
+            a = 0;
+            ++c;
+            if (c < nL) jc = s.listL[c];
+          }
+        }
+      }
+      rbk_combine(s, has, run, s.colsum);
+    }
+    // ---- Eq. 12 finalisation per column ----
+    {
+      double u = 0.0;
+      if (tid < nL) {
+        const double hl = s.hL[tid];
+        const double num = form == 0 ? hl * s.colsum[tid] / N : s.colsum[tid] / (N * hl);
+        u = (num + P.alpha * s.hSc[tid]) / (SR2 / N2 + P.alpha);
+        u = u > 0.0 ? u : 0.0;
+        s.hL1[tid] = u;
+      }
+      slot_put(s, R_SL1, u);
+    }
+    __syncthreads();
+    // ---- Eqs. 15, 14: renormalise; stop test (R11); Eq. 11 refresh is implicit ----
+    {
+      const double SR1 = slot_sum(s, R_SR1), SL1 = slot_sum(s, R_SL1);
+      double dr = 0.0, dl = 0.0, l2 = 0.0;
+      if (tid < nR) {
+        const double n = N * s.hR1[tid] / SR1;
+        dr = (n - s.hR[tid]) * (n - s.hR[tid]);
+        s.hR[tid] = n;
+      }
+      if (tid < nL) {
+        const double n = N * s.hL1[tid] / SL1;
+        dl = (n - s.hL[tid]) * (n - s.hL[tid]);
+        s.hL[tid] = n;
+        l2 = n * n;
+      }
+      s.est[tid] = 0.0;
+      slot_put(s, R_DR, dr);
+      slot_put(s, R_DL, dl);
+      slot_put(s, R_SL2, l2);
+    }
+    __syncthreads();
+    ++t;
+    SL2 = slot_sum(s, R_SL2);
+    const double eps = P.epsilon * N2;
+    const bool conv = P.use_epsilon && slot_sum(s, R_DR) <= eps && slot_sum(s, R_DL) <= eps;
+    if (conv || t >= P.max_iter) break;
+  }
+
+  // ---- outputs hL, hR (dense, zero off support) ----
+  {
+    const int pl = s.posL[tid];
+    const bool inL = s.hSi[tid] != 0u;
+    if (args.hL) args.hL[b * kLevels + tid] = inL ? s.hL[pl] : 0.0;
+    if (args.hR) {
+      // position of tid in listR: scan again (cheap)
+      args.hR[b * kLevels + tid] = 0.0;
+    }
+  }
+  __syncthreads();
+  if (args.hR && tid < nR) args.hR[b * kLevels + s.listR[tid]] = s.hR[tid];
+  if (args.iters && tid == 0) args.iters[b] = t;
+
+  // ---- Eq. 20 with index_1 (Eqs. 17-19): warp per row, segmented by k, warp-private sums ----
+  double* pj = s.hR1;               // p_j = b_j^(1/gamma)   (Eq. 17)
+  double* Twarp = reinterpret_cast<double*>(cells);  // 8 x 256 doubles = 16 KB (cells dead)
+  {
+    const double bj = s.bk[tid];
+    pj[tid] = (P.gamma == 1.0) ? bj : pow(bj, 1.0 / P.gamma);
+    for (int w = 0; w < NW; ++w) Twarp[w * kLevels + tid] = 0.0;
+  }
+  __syncthreads();
+  {
+    const int lane = tid & 31, w = tid >> 5;
+    for (int a = w; a < nR; a += NW) {
+      const double bi = s.bk[s.listR[a]];
+      const double vr = s.hR[a];
+      for (int c0 = 0; c0 < nL; c0 += 32) {
+        const int c = c0 + lane;
+        const bool valid = c < nL;
+        const int k = valid ? idx1(s, bi, pj[s.listL[c]]) : 256 + lane;  // keys non-decreasing
+        double v = valid ? vr * s.hL[c] : 0.0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const double vu = __shfl_up_sync(0xffffffffu, v, d);
+          const int ku = __shfl_up_sync(0xffffffffu, k, d);
+          if (lane >= d && ku == k) v += vu;
+        }
+        const int kn = __shfl_down_sync(0xffffffffu, k, 1);
+        if (valid && (lane == 31 || kn != k)) Twarp[w * kLevels + k] += v;
+      }
+    }
+  }
+  __syncthreads();
+  double* Tt = s.rowsum;  // dense target
+  {
+    double acc = 0.0;
+    for (int w = 0; w < NW; ++w) acc += Twarp[w * kLevels + tid];
+    Tt[tid] = acc / N;
+    if (args.target) args.target[b * kLevels + tid] = Tt[tid];
+  }
+  __syncthreads();
+  if (args.lut || args.status)
+    cdf_lut(s.hSi, Tt, s.colsum, s.est, s.rho, wscr, args.lut ? args.lut + b * kLevels : nullptr,
+            args.status ? args.status + b : nullptr);
+}
+
+__global__ void __launch_bounds__(T) k_remap(const uint32_t* graw, int32_t grad_norm, uint32_t* hist_g) {
+  __shared__ uint32_t h[kLevels];
+  __shared__ int wscr[NW];
+  const int64_t b = blockIdx.x;
+  remap_gradient(graw + b * kGradSlots, grad_norm, h, wscr);
+  hist_g[b * kLevels + threadIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(T) k_match(const uint32_t* hist_s, const double* target, uint8_t* lut,
+                                             int32_t* status) {
+  __shared__ uint32_t hSi[kLevels];
+  __shared__ double Tt[kLevels], Pt[kLevels], Ct[kLevels], Cs[kLevels];
+  __shared__ int wscr[NW];
+  const int64_t b = blockIdx.x;
+  hSi[threadIdx.x] = hist_s[b * kLevels + threadIdx.x];
+  Tt[threadIdx.x] = target[b * kLevels + threadIdx.x];
+  __syncthreads();
+  cdf_lut(hSi, Tt, Pt, Ct, Cs, wscr, lut + b * kLevels, status ? status + b : nullptr);
+}
+
+}  // namespace
+
+size_t solve_smem_bytes() { return sizeof(Sm) + (size_t)kMaxCells * sizeof(uint16_t); }
+
+cudaError_t launch_solve(const SolveArgs& a, int64_t B, cudaStream_t st) {
+  static bool attr = false;
+  const size_t smem = solve_smem_bytes();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_solve<<<(unsigned)B, T, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_remap(const uint32_t* hist_graw, int64_t B, int32_t grad_norm, uint32_t* hist_g,
+                         cudaStream_t st) {
+  k_remap<<<(unsigned)B, T, 0, st>>>(hist_graw, grad_norm, hist_g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,
+                         int32_t* status, cudaStream_t st) {
+  k_match<<<(unsigned)B, T, 0, st>>>(hist_s, target, lut, status);
+  return cudaGetLastError();
+}
+
+}  // namespace hr

@@ -1,0 +1,333 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Bar: histograms, raw gradient histograms, LUTs, iteration counts and
+output pixels bit-exact; hL, hR, target within 1e-4 relative per nonzero bin (the
+north-star tolerance; measured values are ~1e-13) and exactly zero on zero bins.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4  # BASELINE.json north_star: "within 1e-4 relative per bin"
+NTHREADS = max(1, min(32, os.cpu_count() or 1))
+
+
+def hr():
+    import paper_2510_21100_b200 as m
+
+    return m
+
+
+def P(**kw):
+    return hr().Params(**kw), oracle.Params(**kw)
+
+
+PARAM_SETS = {
+    "default": dict(),  # MAXNORM, alpha 0.1, beta 1e-3, gamma 2.2
+    "spec_literal": dict(grad_norm=1, alpha=0.1, beta=0.1),
+    "gamma1": dict(gamma=1.0),
+    "paper_form": dict(update_form=1),
+    "eps_rule": dict(use_epsilon=1, epsilon=1e-3),
+    "gamma5_beta01": dict(gamma=5.0, beta=0.1),
+}
+
+
+def rel_err(gpu, ref):
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    nz = ref != 0
+    assert np.all(gpu[~nz] == 0.0), "nonzero where the oracle is exactly zero"
+    if not nz.any():
+        return 0.0
+    return float(np.max(np.abs(gpu[nz] - ref[nz]) / np.abs(ref[nz])))
+
+
+def to_dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def check_enhance(x, pset="default", sample_pixels=None):
+    hp, op = P(**PARAM_SETS[pset])
+    xd = to_dev(x)
+    out, hs, lut, it = hr().hr_enhance_debug(xd, hp)
+    torch.cuda.synchronize()
+    out, hs, lut, it = out.cpu().numpy(), hs.cpu().numpy(), lut.cpu().numpy(), it.cpu().numpy()
+    B = x.shape[0]
+    for b in range(B):
+        r = oracle.enhance(x[b], op)
+        assert np.array_equal(hs[b].astype(np.uint64), r.hS), f"hist_s image {b}"
+        assert it[b] == r.iters, f"iters image {b}: {it[b]} vs {r.iters}"
+        check_lut(lut[b].astype(np.int32), r, f"image {b}")
+        if np.array_equal(lut[b].astype(np.int32), r.lut):
+            assert np.array_equal(out[b], r.out), f"pixels image {b}: {np.count_nonzero(out[b] != r.out)} differ"
+        else:  # rounding-level ties: pixels must follow the GPU's (valid) LUT exactly
+            ref = oracle.reconstruct(x[b].reshape(-1, 3), lut[b].astype(np.int32)[x[b].reshape(-1, 3).max(-1)])
+            assert np.array_equal(out[b].reshape(-1, 3), ref)
+    return out
+
+
+TIE_TOL = 1e-12  # CDF units; oracle decision margins below this are fp64 rounding-level ties
+
+
+def check_lut(gpu_lut, r, what):
+    """LUT bit-exact wherever the oracle's decision margin exceeds TIE_TOL; at rounding-level
+    ties (margin <= TIE_TOL, the two nearest CDF values are equal to within fp64 rounding) the
+    GPU entry must be a valid argmin: its distance within TIE_TOL of the minimum."""
+    bad = np.nonzero(gpu_lut != r.lut)[0]
+    if bad.size == 0:
+        return 0
+    Pt = np.cumsum(r.T)
+    Ct = Pt / Pt[-1]
+    Cs = np.cumsum(r.hS.astype(np.float64)) / float(r.hS.sum())
+    for v in bad:
+        assert r.margin[v] <= TIE_TOL, f"lut {what}: level {v} gpu {gpu_lut[v]} oracle {r.lut[v]} margin {r.margin[v]}"
+        d = np.abs(Ct - Cs[v])
+        assert d[gpu_lut[v]] <= d.min() + TIE_TOL, f"lut {what}: level {v} gpu choice not an argmin"
+    assert np.all(np.diff(gpu_lut) >= 0)
+    print(f"{what}: {bad.size} LUT entries decided by fp64 rounding-level ties (margin <= {TIE_TOL})")
+    return bad.size
+
+
+# ------------------------------------------------------------- step (1)
+@pytest.mark.parametrize("name", list(synth.edge_images().keys()))
+def test_histogram_edge_images(name):
+    img = synth.edge_images()[name][None]
+    for gn in (0, 1):
+        hs, hg, hgr = hr().hr_histogram(to_dev(img), grad_norm=gn)
+        r = oracle.enhance(img[0], oracle.Params(grad_norm=gn))
+        assert np.array_equal(hs.cpu().numpy()[0].astype(np.uint64), r.hS)
+        assert np.array_equal(hg.cpu().numpy()[0].astype(np.uint64), r.hG)
+        assert np.array_equal(hgr.cpu().numpy()[0, :511].astype(np.uint64), r.hgraw)
+        assert hgr.cpu().numpy()[0, 511] == 0
+
+
+@pytest.mark.parametrize("cfg,batch", [("C1", None), ("C2", None), ("C5", 7), ("C3", 2)])
+def test_histogram_configs(cfg, batch):
+    x = synth.make_config(cfg, batch=batch)
+    hs, hg, hgr = hr().hr_histogram(to_dev(x))
+    hs, hg, hgr = hs.cpu().numpy(), hg.cpu().numpy(), hgr.cpu().numpy()
+    for b in range(x.shape[0]):
+        S = oracle.value_channel(x[b])
+        g = oracle.gradient_raw(S)
+        assert np.array_equal(hs[b].astype(np.uint64), oracle.count_histogram(S, 256))
+        assert np.array_equal(hgr[b, :511].astype(np.uint64), oracle.count_histogram(g, 511))
+        assert np.array_equal(hg[b].astype(np.uint64),
+                              oracle.count_histogram(oracle.gradient_levels(g, 256, 0), 256))
+
+
+@pytest.mark.parametrize("shape", [(3, 37, 101), (2, 1, 173), (2, 157, 1), (4, 16, 16), (1, 5, 8200)])
+def test_histogram_ragged_shapes(shape):
+    B, H, W = shape
+    x = np.stack([synth.make_image(H, W, seed=100 + b, peak=0.05 + 0.1 * b) for b in range(B)])
+    hs, hg, hgr = hr().hr_histogram(to_dev(x))
+    for b in range(B):
+        S = oracle.value_channel(x[b])
+        g = oracle.gradient_raw(S)
+        assert np.array_equal(hs.cpu().numpy()[b].astype(np.uint64), oracle.count_histogram(S, 256))
+        assert np.array_equal(hgr.cpu().numpy()[b, :511].astype(np.uint64), oracle.count_histogram(g, 511))
+
+
+def test_histogram_unaligned_base():
+    x = synth.make_image(40, 64, seed=5)
+    buf = torch.zeros(40 * 64 * 3 + 1, dtype=torch.uint8, device="cuda")
+    buf[1:] = to_dev(x).reshape(-1)
+    xd = buf[1:].view(1, 40, 64, 3)  # 1-byte misaligned base
+    hs, hg, hgr = hr().hr_histogram(xd)
+    S = oracle.value_channel(x)
+    assert np.array_equal(hs.cpu().numpy()[0].astype(np.uint64), oracle.count_histogram(S, 256))
+    assert np.array_equal(hgr.cpu().numpy()[0, :511].astype(np.uint64),
+                          oracle.count_histogram(oracle.gradient_raw(S), 511))
+
+
+# ------------------------------------------------------------- step (2)
+@pytest.mark.parametrize("pset", list(PARAM_SETS))
+def test_solve_vs_oracle(pset):
+    hp, op = P(**PARAM_SETS[pset])
+    imgs = [synth.make_image(120, 160, seed=7), synth.make_config("C5", batch=1)[0][:200, :300],
+            synth.edge_images()["uniform_noise"], synth.make_image(90, 70, seed=8, peak=0.4)]
+    hs_l, hg_l, refs = [], [], []
+    for im in imgs:
+        r = oracle.enhance(im, op)
+        hs_l.append(r.hS.astype(np.int32))
+        hg_l.append(r.hG.astype(np.int32))
+        refs.append(r)
+    hL, hR, tg, it = hr().hr_solve(to_dev(np.stack(hs_l)), to_dev(np.stack(hg_l)), hp)
+    hL, hR, tg, it = (t.cpu().numpy() for t in (hL, hR, tg, it))
+    worst = 0.0
+    for b, r in enumerate(refs):
+        assert it[b] == r.iters
+        worst = max(worst, rel_err(hL[b], r.hL), rel_err(hR[b], r.hR), rel_err(tg[b], r.T))
+    print(f"[{pset}] max relative error hL/hR/target vs fp64 oracle: {worst:.3e}")
+    assert worst <= RTOL
+
+
+def test_solve_deterministic():
+    x = synth.make_config("C5", batch=8)
+    hs, hg, _ = hr().hr_histogram(to_dev(x))
+    a = hr().hr_solve(hs, hg)
+    b = hr().hr_solve(hs, hg)
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
+
+
+# ------------------------------------------------------------- step (3)
+def test_match_vs_oracle():
+    imgs = [synth.make_image(100, 150, seed=s, peak=p) for s, p in ((1, 0.3), (2, 0.05), (3, 0.4))]
+    rs = [oracle.enhance(im) for im in imgs]
+    hs = to_dev(np.stack([r.hS.astype(np.int32) for r in rs]))
+    tg = to_dev(np.stack([r.T for r in rs]))
+    lut, st = hr().hr_match(hs, tg)
+    lut = lut.cpu().numpy()
+    assert np.all(st.cpu().numpy() == 0)
+    for b, r in enumerate(rs):
+        assert np.array_equal(lut[b].astype(np.int32), r.lut)
+        assert np.all(np.diff(lut[b].astype(np.int32)) >= 0)
+
+
+def test_match_degenerate_status():
+    hs = torch.ones((1, 256), dtype=torch.int32, device="cuda")
+    tg = torch.zeros((1, 256), dtype=torch.float64, device="cuda")
+    lut, st = hr().hr_match(hs, tg)
+    assert st.item() == 3
+    assert torch.equal(lut[0].long(), torch.arange(256, device="cuda"))
+
+
+def test_match_bruteforce_random_targets():
+    rng = np.random.default_rng(3)
+    hs = rng.integers(0, 50, size=(16, 256)) * (rng.random((16, 256)) < 0.5)
+    hs[:, 7] += 1
+    tg = rng.random((16, 256)) * (rng.random((16, 256)) < 0.4)
+    tg[:, 200] += 0.5
+    lut, _ = hr().hr_match(to_dev(hs.astype(np.int32)), to_dev(tg))
+    lut = lut.cpu().numpy()
+    for b in range(16):
+        assert np.array_equal(lut[b].astype(np.int32), oracle.match_lut(hs[b].astype(np.uint64), tg[b]))
+
+
+# ------------------------------------------------------------- step (4)
+def test_apply_exhaustive_pixels():
+    """Every (R,G,B) on a grid x every V' through random LUTs, vs the exact hexcone oracle."""
+    vals = np.array([0, 1, 2, 3, 5, 17, 64, 100, 127, 128, 200, 254, 255], np.uint8)
+    R, G, B = np.meshgrid(vals, vals, vals, indexing="ij")
+    px = np.stack([R.ravel(), G.ravel(), B.ravel()], -1)
+    rng = np.random.default_rng(0)
+    x = np.tile(px, (8, 1))[None, None].reshape(1, 1, -1, 3)
+    x = np.concatenate([x, rng.integers(0, 256, size=(1, 1, 30000, 3), dtype=np.uint8)], axis=2)
+    for _ in range(4):
+        lut = np.sort(rng.integers(0, 256, size=256)).astype(np.uint8)
+        out = hr().hr_apply(to_dev(x), to_dev(lut[None])).cpu().numpy()
+        V = x[0, 0].max(-1)
+        ref = oracle.reconstruct(x[0, 0], lut[V].astype(np.int32))
+        assert np.array_equal(out[0, 0], ref)
+
+
+def test_apply_in_place_and_ragged():
+    x = synth.make_image(37, 101, seed=9)[None]
+    lut = np.arange(256, dtype=np.uint8)[::-1].copy()
+    xd = to_dev(x)
+    ref = oracle.reconstruct(x[0].reshape(-1, 3), lut[x[0].reshape(-1, 3).max(-1)].astype(np.int32))
+    out = hr().hr_apply(xd, to_dev(lut[None]), out=xd)
+    assert np.array_equal(out.cpu().numpy().reshape(-1, 3), ref)
+
+
+# ------------------------------------------------------------- (1)-(4)
+@pytest.mark.parametrize("name", list(synth.edge_images().keys()))
+def test_enhance_edge_images(name):
+    check_enhance(synth.edge_images()[name][None])
+
+
+@pytest.mark.parametrize("pset", list(PARAM_SETS))
+def test_enhance_c1_param_sets(pset):
+    check_enhance(synth.make_config("C1"), pset)
+
+
+def test_enhance_c1_default_eps_rule():
+    # C1 is quoted with the Alg. 1 stop rule (BASELINE.json configs[0])
+    check_enhance(synth.make_config("C1"), "eps_rule")
+
+
+def test_enhance_c2_full():
+    check_enhance(synth.make_config("C2"))
+
+
+def test_enhance_mixed_batch_no_leakage():
+    x = np.stack([synth.make_image(60, 80, seed=s, peak=p) for s, p in ((1, 0.03), (2, 0.3), (3, 0.05))])
+    check_enhance(x)
+
+
+def test_enhance_determinism():
+    x = to_dev(synth.make_config("C5", batch=16))
+    a = hr().hr_enhance(x)
+    b = hr().hr_enhance(x)
+    assert torch.equal(a, b)
+
+
+def _sampled_full_check(x, sample_images, n_px=200000):
+    """Full-size batch on the GPU (bench launch configuration); oracle on a sample of images,
+    all histograms/LUTs of the sample and a random pixel sample of each."""
+    hp, op = P()
+    xd = to_dev(x)
+    out, hs, lut, it = hr().hr_enhance_debug(xd, hp)
+    torch.cuda.synchronize()
+    out_d = out
+    hs, lut, it = hs.cpu().numpy(), lut.cpu().numpy(), it.cpu().numpy()
+    ref = oracle.enhance_batch(x[sample_images], op, nthreads=NTHREADS, want_out=False)
+    rng = np.random.default_rng(0)
+    for k, b in enumerate(sample_images):
+        assert np.array_equal(hs[b].astype(np.uint64), ref["hS"][k])
+        assert it[b] == ref["iters"][k]
+        assert np.array_equal(lut[b].astype(np.int32), ref["lut"][k]), f"image {b}"
+        flat = x[b].reshape(-1, 3)
+        idx = rng.choice(flat.shape[0], size=min(n_px, flat.shape[0]), replace=False)
+        idx_t = torch.from_numpy(idx).cuda()
+        got = out_d[b].reshape(-1, 3)[idx_t].cpu().numpy()
+        exp = oracle.reconstruct(flat[idx], ref["lut"][k][flat[idx].max(-1)])
+        assert np.array_equal(got, exp)
+
+
+def test_enhance_c3_full_size_sampled():
+    x = synth.make_config("C3")
+    _sampled_full_check(x, [0, 17, 40, 63])
+
+
+def test_enhance_c5_full_size_sampled():
+    x = synth.make_config("C5")
+    _sampled_full_check(x, [0, 1, 100, 200, 255])
+
+
+def test_enhance_c4_full_size_sampled():
+    x = synth.make_config("C4")
+    _sampled_full_check(x, [0], n_px=300000)
+
+
+def test_enhance_c5_full_batch_every_lut():
+    """Every image of C5: histograms, iterations and LUTs bit-exact."""
+    x = synth.make_config("C5")
+    hp, op = P()
+    out, hs, lut, it = hr().hr_enhance_debug(to_dev(x), hp)
+    ref = oracle.enhance_batch(x, op, nthreads=NTHREADS, want_out=False)
+    assert np.array_equal(hs.cpu().numpy().astype(np.uint64), ref["hS"])
+    assert np.array_equal(it.cpu().numpy(), ref["iters"])
+    assert np.array_equal(lut.cpu().numpy().astype(np.int32), ref["lut"])
+
+
+# ------------------------------------------------------------- errors
+def test_errors_are_raised():
+    m = hr()
+    x = to_dev(synth.make_image(8, 8, seed=1)[None])
+    with pytest.raises(m.HrError) as e:
+        m.hr_enhance(x, m.Params(gamma=0.5))
+    assert e.value.status == 1
+    with pytest.raises(m.HrError) as e:
+        m.hr_enhance(x, m.Params(levels=128))
+    assert e.value.status == 5
+    with pytest.raises(m.HrError) as e:
+        m.hr_enhance(torch.zeros((1, 0, 5, 3), dtype=torch.uint8, device="cuda"))
+    assert e.value.status == 2
