@@ -29,7 +29,7 @@ using hr::kLevels;
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WsLayout {
-  size_t hist_s, graw, lut, iters, total;
+  size_t hist_s, graw, lut, iters, cells, total;
 };
 
 WsLayout ws_layout(int64_t B) {
@@ -43,6 +43,8 @@ WsLayout ws_layout(int64_t B) {
   o = align_up(o + (size_t)B * kLevels);
   L.iters = o;
   o = align_up(o + (size_t)B * sizeof(int32_t));
+  L.cells = o;
+  o = align_up(o + hr::solve_cells_ws_bytes(B));
   L.total = o;
   return L;
 }
@@ -91,7 +93,7 @@ hr_status activate(hr_ctx* c) {
 }
 
 int hist_grid(const hr_ctx* c) { return 2 * c->num_sms; }
-int apply_grid(const hr_ctx* c) { return 8 * c->num_sms; }
+int apply_grid(const hr_ctx* c) { return c->num_sms; }  // launch_apply sizes its own grid
 
 }  // namespace
 
@@ -214,13 +216,13 @@ hr_status hr_histogram(hr_ctx* c, const uint8_t* rgb, int64_t B, int32_t H, int3
 hr_status hr_solve(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, int64_t B, const hr_params* p,
                    double* hL, double* hR, double* target, int32_t* iters, void* ws, void* stream) {
   if (!c) return HR_EINVAL;
-  if (!hist_s || !hist_g || !hL || !hR || !target) return set_err(c, HR_EINVAL, "NULL pointer");
+  if (!hist_s || !hist_g || !hL || !hR || !target || !ws) return set_err(c, HR_EINVAL, "NULL pointer");
   if (B < 1 || B > (1 << 30)) return set_err(c, HR_EINVAL, "B must be >= 1");
   hr_status s = check_params(c, p);
   if (s) return s;
   if ((s = activate(c))) return s;
-  (void)ws;
   hr::SolveArgs a{};
+  a.cells_ws = reinterpret_cast<uint16_t*>((char*)ws + ws_layout(B).cells);
   a.hist_s = hist_s;
   a.hist_g = hist_g;
   a.graw = nullptr;
@@ -297,6 +299,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     a.p = *p;
     a.iters = iters_dbg;
     a.lut = lut;
+    a.cells_ws = reinterpret_cast<uint16_t*>((char*)ws + L.cells);
     e = hr::launch_solve(a, B, st);
   }
   if (e == cudaSuccess) e = mark(2);

@@ -45,14 +45,16 @@ struct SolveArgs {
   int32_t* iters;           // [B] nullable
   uint8_t* lut;             // [B][256] nullable (fused CDF + LUT tail)
   int32_t* status;          // [B] nullable
+  uint16_t* cells_ws;       // [B][65536] cell lists of images whose supports exceed shared memory
 };
 cudaError_t launch_solve(const SolveArgs& a, int64_t B, cudaStream_t st);
 size_t solve_smem_bytes();
+size_t solve_cells_ws_bytes(int64_t B);
 
 cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,
                          int32_t* status, cudaStream_t st);
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
-                         uint8_t* out, int grid, cudaStream_t st);
+                         uint8_t* out, int num_sms, cudaStream_t st);
 
 }  // namespace hr

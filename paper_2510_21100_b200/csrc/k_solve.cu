@@ -1,7 +1,7 @@
 // k_solve.cu -- kernel (b): batched histogram-domain Retinex solver (Algorithm 1) in fp64,
 // with the Eq. 17-20 reprocessing and the fused CDF + histogram-matching LUT tail (c).
 //
-// One CTA (256 threads) per image.  PAPER.md references:
+// One CTA (256 threads) per image, 2 CTAs per SM.  PAPER.md references:
 //   Eq. 6  count matrix  C_ij = hR_i hL_j / N          -- never materialised
 //   Eq. 7  location matrix b_i b_j (R1, R2)            -- constant: idx(i,j)
 //   P:192           index(i,j) = nearest bin of b_i b_j          = (i*j + 127) div 255
@@ -19,9 +19,16 @@
 //   Paper-literal form (K_ij as a divisor): A_i = sum_j sigma_k / hR_i, sigma_k = hS_k EstRaw_k,
 //        B_j = sum_i (hR'_i / hR_i) sigma_k / hL_j   (both divided by N).
 // Supports never change (hR stays 0 off supp(hG), hL off supp(hS)), so every pass runs over
-// the compacted cells sR x sL only.  All reductions are fixed-order (reduce-by-key over
-// per-thread slices + a deterministic segmented scan): results are bit-identical run to
-// run; no floating-point atomics anywhere.
+// the E = nR x nL compacted cells only.
+//
+// Each of the three passes (E: cells grouped by output bin k; R: row-major, key = row;
+// L: column-major, key = column) is a segmented sum whose segment boundaries are known in
+// advance.  Thread t sums the fixed slice [t*S, t*S+S) of the pass's cell order: segments
+// wholly inside its slice are finalised by the thread itself; a segment spanning several
+// slices leaves a partial in pf[t] (its part at the slice start) / pl[t] (at the slice end),
+// and after one barrier the segment's owner adds those partials in slice order.  Two
+// barriers per pass, no floating-point atomics, a fixed summation order: bit-identical run
+// to run.
 #include "hr_common.cuh"
 
 namespace hr {
@@ -30,36 +37,32 @@ namespace {
 constexpr int T = kSolveThreads;
 constexpr int NW = kSolveWarps;
 constexpr int kMaxCells = kLevels * kLevels;
+constexpr int kSmemCells = 32768;  // cell list capacity in shared memory (64 KB)
 
 // slots of the block-reduction scratch
-enum { R_SL2 = 0, R_SR1, R_SR2, R_SL1, R_DR, R_DL, R_N, kSlots };
+enum { R_SL2 = 0, R_SR1, R_SR2, R_SL1, R_DR, R_DL, kSlots };
 
 struct __align__(16) Sm {
   double hR[kLevels], hL[kLevels];    // compacted state (index a over sR, c over sL)
   double hR1[kLevels], hL1[kLevels];  // raw updates (Eq. 13 / Eq. 12 outputs)
   double hSc[kLevels], hGc[kLevels];  // priors at the support entries
+  double hL2[kLevels];                // hL_c^2
   double wgt[kLevels];                // per-row weight of the L-pass
   double hSd[kLevels];                // dense hS as double
   double est[kLevels];                // EstRaw_k (= N Est_k)
   double rho[kLevels];                // rho_k (GC) or sigma_k (paper-literal)
-  double rowsum[kLevels], colsum[kLevels];
   double bk[kLevels];                 // b_k = k/255 (R1)
+  double pf[T], pl[T];                // slice-boundary partials
   double red[kSlots][NW];
-  // reduce-by-key scratch
-  double sfA[T], slA[T], outA[T];
-  double wv[NW];
-  int kfA[T], klA[T];
-  int wf[NW];
-  uint8_t hasA[T];
-  // supports
   uint32_t hSi[kLevels], hGi[kLevels];
+  uint32_t rcp[kLevels];              // ceil(2^32 / i)
   int cstart[kLevels + 1];
   uint16_t posL[kLevels + 1];
   uint8_t listR[kLevels], listL[kLevels];
   int nR, nL, E;
-  uint64_t Nint;
+  unsigned long long Nint;
+  unsigned long long nw[NW];
 };
-// the Eq. 20 pass and the CDF tail reuse the iteration arrays (dead by then)
 
 __device__ __forceinline__ int idx0(int i, int j) {  // P:192 index(i,j) for l = 256
   return (int)(((uint32_t)(i * j + 127) * 32897u) >> 23);
@@ -84,83 +87,6 @@ __device__ __forceinline__ void slot_put(Sm& s, int slot, double v) {
   if ((threadIdx.x & 31) == 0) s.red[slot][threadIdx.x >> 5] = v;
 }
 
-// Per-thread run accumulator for reduce-by-key over a contiguous slice whose keys are
-// non-decreasing.  Runs strictly inside the slice are owned by this thread and written
-// directly; the first and last runs may continue into neighbouring slices.
-struct Runs {
-  int cur, kf;
-  double acc, sf;
-  bool first;
-  __device__ __forceinline__ void begin(int k, double v) {
-    cur = k;
-    acc = v;
-    first = true;
-  }
-  __device__ __forceinline__ void step(int k, double v, double* out) {
-    if (k == cur) {
-      acc += v;
-    } else {
-      if (first) {
-        kf = cur;
-        sf = acc;
-        first = false;
-      } else {
-        out[cur] = acc;
-      }
-      cur = k;
-      acc = v;
-    }
-  }
-};
-
-// Deterministic combination of the per-thread boundary runs (segmented scan over threads).
-// On return (after the trailing barrier) out[key] holds the full sum of every key that
-// occurs in the slices.
-__device__ void rbk_combine(Sm& s, bool has, const Runs& r, double* out) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const bool single = has && r.first;
-  const int kf = has ? (single ? r.cur : r.kf) : -1;
-  const double sf = has ? (single ? r.acc : r.sf) : 0.0;
-  const int kl = has ? r.cur : -2;
-  const double sl = has ? r.acc : 0.0;
-  s.kfA[tid] = kf;
-  s.klA[tid] = kl;
-  s.hasA[tid] = has;
-  __syncthreads();
-  const bool prevHas = tid > 0 && s.hasA[tid - 1];
-  const bool prevSame = prevHas && s.klA[tid - 1] == kf;
-  bool f = !(has && single && prevSame);  // head of a chain of single-key slices
-  double v = sl;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const double vu = __shfl_up_sync(0xffffffffu, v, d);
-    const bool fu = __shfl_up_sync(0xffffffffu, (int)f, d) != 0;
-    if (lane >= d) {
-      if (!f) v = vu + v;
-      f = f || fu;
-    }
-  }
-  if (lane == 31) {
-    s.wv[w] = v;
-    s.wf[w] = f;
-  }
-  __syncthreads();
-  if (!f) {
-    double cv = 0.0;
-    for (int u = 0; u < w; ++u) cv = s.wf[u] ? s.wv[u] : cv + s.wv[u];
-    v = cv + v;
-  }
-  s.outA[tid] = v;
-  __syncthreads();
-  if (has) {
-    if (!single) out[kf] = sf + (prevSame ? s.outA[tid - 1] : 0.0);
-    const bool nextCont = tid + 1 < T && s.hasA[tid + 1] && s.kfA[tid + 1] == kl;
-    if (!nextCont) out[kl] = v;
-  }
-  __syncthreads();
-}
-
-// inclusive block scan of non-negative ints (exact)
 __device__ int block_scan_excl(int x, int* total, int* wscratch) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int v = x;
@@ -181,7 +107,12 @@ __device__ int block_scan_excl(int x, int* total, int* wscratch) {
   return off + v - x;
 }
 
-// c-range [lo, hi] of the compacted columns whose index(i, j) == k (idx monotone in j)
+// c-range [lo, hi] of the compacted columns whose index(i, j) == k (idx monotone in j).
+// Divisions by i use the exact reciprocal magic floor(x / i) = umulhi(x, ceil(2^32 / i))
+// (x <= 65152, i <= 255: error x (ceil - 2^32/i) / 2^32 < 1/i).
+__device__ __forceinline__ int div_i(const Sm& s, uint32_t x, int i) {
+  return i == 1 ? (int)x : (int)__umulhi(x, s.rcp[i]);
+}
 __device__ __forceinline__ void crange(const Sm& s, int i, int k, int& lo, int& hi) {
   if (i == 0) {  // index(0, j) = 0 for all j
     lo = 0;
@@ -190,8 +121,8 @@ __device__ __forceinline__ void crange(const Sm& s, int i, int k, int& lo, int& 
   }
   // (i*j + 127) div 255 == k  <=>  255k - 127 <= i*j <= 255k + 127
   const int a = 255 * k - 127, bnd = 255 * k + 127;
-  int jlo = a <= 0 ? 0 : (a + i - 1) / i;
-  int jhi = bnd / i;
+  const int jlo = a <= 0 ? 0 : div_i(s, (uint32_t)(a + i - 1), i);
+  int jhi = div_i(s, (uint32_t)bnd, i);
   if (jhi > 255) jhi = 255;
   if (jlo > jhi) {
     lo = 0;
@@ -315,7 +246,17 @@ __device__ void remap_gradient(const uint32_t* graw, int grad_norm, uint32_t* hG
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
+// Sum of the partials of a segment [ks, ke) that spans slices t1 < t2 (slice size S).
+__device__ __forceinline__ double span_sum(const Sm& s, int ks, int ke, int S) {
+  const int t1 = ks / S, t2 = (ke - 1) / S;
+  double acc = s.pl[t1];
+  for (int t = t1 + 1; t < t2; ++t) acc += s.pf[t];
+  return acc + s.pf[t2];
+}
+
+__device__ __forceinline__ bool spans(int ks, int ke, int S) { return ks / S != (ke - 1) / S; }
+
+__global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
   extern __shared__ __align__(16) unsigned char smraw[];
   Sm& s = *reinterpret_cast<Sm*>(smraw);
   uint16_t* cells = reinterpret_cast<uint16_t*>(smraw + sizeof(Sm));
@@ -333,6 +274,8 @@ __global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
   }
   s.bk[tid] = (double)tid / 255.0;
   s.hSd[tid] = (double)s.hSi[tid];
+  s.rcp[tid] = tid <= 1 ? 0u : (uint32_t)((0x100000000ull + (uint64_t)tid - 1) / (uint64_t)tid);
+  s.est[tid] = 0.0;
   __syncthreads();
 
   // ---- supports (fixed for all t) ----
@@ -343,28 +286,22 @@ __global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
   if (fL) s.listL[pL] = (uint8_t)tid;
   if (fR) s.listR[pR] = (uint8_t)tid;
   s.posL[tid] = (uint16_t)pL;
+  {
+    unsigned long long v = s.hSi[tid];
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if ((tid & 31) == 0) s.nw[tid >> 5] = v;
+  }
   if (tid == 0) {
     s.posL[kLevels] = (uint16_t)nL;
     s.nL = nL;
     s.nR = nR;
   }
-  // N = sum hS (exact integer)
-  {
-    unsigned long long v = s.hSi[tid];
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    __shared__ unsigned long long nw[NW];
-    if ((tid & 31) == 0) nw[tid >> 5] = v;
-    __syncthreads();
-    if (tid == 0) {
-      unsigned long long n = 0;
-      for (int u = 0; u < NW; ++u) n += nw[u];
-      s.Nint = n;
-    }
-  }
   __syncthreads();
-  const double N = (double)s.Nint;
-  if (s.Nint == 0 || nR == 0) {  // empty image: zero outputs (never for validated inputs)
+  unsigned long long Nint = 0;
+  for (int u = 0; u < NW; ++u) Nint += s.nw[u];
+  const double N = (double)Nint;
+  if (Nint == 0 || nR == 0) {  // empty image: zero outputs (never for validated inputs)
     if (args.hL) args.hL[b * kLevels + tid] = 0.0;
     if (args.hR) args.hR[b * kLevels + tid] = 0.0;
     if (args.target) args.target[b * kLevels + tid] = 0.0;
@@ -377,19 +314,24 @@ __global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
   }
 
   // ---- compacted state: hR^0 = hG, hL^0 = hS (R9) ----
+  double l2 = 0.0;
   if (tid < nL) {
     const double v = s.hSd[s.listL[tid]];
     s.hL[tid] = v;
     s.hSc[tid] = v;
+    s.hL2[tid] = v * v;
+    l2 = v * v;
   }
   if (tid < nR) {
     const double v = (double)s.hGi[s.listR[tid]];
     s.hR[tid] = v;
     s.hGc[tid] = v;
   }
-  s.est[tid] = 0.0;
+  slot_put(s, R_SL2, l2);
 
-  // ---- cells sorted by output bin k = index(i,j): one thread per k ----
+  // ---- cells grouped by output bin k = index(i,j): one thread per k ----
+  const int E = nR * nL;  // every cell of sR x sL has exactly one k
+  uint16_t* cl = (E <= kSmemCells || args.cells_ws == nullptr) ? cells : args.cells_ws + b * kMaxCells;
   {
     const int k = tid;
     int cnt = 0;
@@ -398,142 +340,161 @@ __global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
       crange(s, s.listR[a], k, lo, hi);
       if (hi >= lo) cnt += hi - lo + 1;
     }
-    int E;
-    const int start = block_scan_excl(cnt, &E, wscr);
+    int Etot;
+    const int start = block_scan_excl(cnt, &Etot, wscr);
     s.cstart[k] = start;
-    if (tid == 0) {
-      s.cstart[kLevels] = E;
-      s.E = E;
-    }
+    if (tid == 0) s.cstart[kLevels] = Etot;
     int pos = start;
-    for (int a = 0; a < nR; ++a) {
+    for (int a = 0; a < nR && pos < start + cnt; ++a) {
       int lo, hi;
       crange(s, s.listR[a], k, lo, hi);
-      for (int c = lo; c <= hi; ++c) cells[pos++] = (uint16_t)((a << 8) | c);
+      for (int c = lo; c <= hi; ++c) cl[pos++] = (uint16_t)((a << 8) | c);
     }
-  }
-  {
-    double v = tid < nL ? s.hL[tid] * s.hL[tid] : 0.0;
-    slot_put(s, R_SL2, v);
   }
   __syncthreads();
 
-  const int E = s.E;
-  const int ER = nR * nL;  // == E (every cell of sR x sL has exactly one k)
   const double N2 = N * N;
   const int form = P.update_form;
-  // E-pass slice and its first key (fixed for all iterations)
-  const int SE = (E + T - 1) / T;
-  const int e0 = min(E, tid * SE), e1 = min(E, e0 + SE);
-  int kstart = 0;
-  if (e0 < e1) {
-    int lo = 0, hi = kLevels + 1;  // upper_bound(cstart, e0) - 1
+  const int S = (E + T - 1) / T;            // slice length, identical for the three passes
+  const int e0 = min(E, tid * S), e1 = min(E, e0 + S);
+  const bool has = e0 < e1;
+  int kstart = 0;                           // bin of cell e0 in the k-grouped order
+  if (has) {
+    int lo = 0, hi = kLevels + 1;           // upper_bound(cstart, e0) - 1
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (s.cstart[mid] <= e0) lo = mid + 1; else hi = mid;
     }
     kstart = lo - 1;
   }
-  const int SRW = (ER + T - 1) / T;
-  const int r0 = min(ER, tid * SRW), r1 = min(ER, r0 + SRW);
+  const int astart = has ? e0 / nL : 0;     // row of cell e0 (row-major)
+  const int cstart0 = has ? e0 / nR : 0;    // column of cell e0 (column-major)
 
   double SL2 = slot_sum(s, R_SL2);
   int t = 0;
   for (;;) {
-    // ---- E-pass: EstRaw_k = sum_{idx=k} hR_a hL_c  (Eq. 6 + Eq. 8 with N folded) ----
-    {
-      Runs run;
-      const bool has = e0 < e1;
-      if (has) {
-        int k = kstart;
-        for (int e = e0; e < e1; ++e) {
-          while (e >= s.cstart[k + 1]) ++k;
-          const uint32_t cl = cells[e];
-          const double v = s.hR[cl >> 8] * s.hL[cl & 255];
-          if (e == e0) run.begin(k, v); else run.step(k, v, s.est);
+    // ======== E-pass: EstRaw_k = sum_{idx=k} hR_a hL_c  (Eqs. 6, 8 with N folded) ========
+    if (has) {
+      int k = kstart;
+      for (;;) {
+        const int ks = s.cstart[k], ke = s.cstart[k + 1];
+        const int lo = max(ks, e0), hi = min(ke, e1);
+        double acc = 0.0;
+        for (int e = lo; e < hi; ++e) {
+          const uint32_t x = cl[e];
+          acc += s.hR[x >> 8] * s.hL[x & 255u];
         }
+        if (ks >= e0 && ke <= e1) {
+          s.est[k] = acc;
+          s.rho[k] = form == 0 ? (acc > 0.0 ? s.hSd[k] / acc : 0.0) : s.hSd[k] * acc;
+        } else {
+          if (ks < e0) s.pf[tid] = acc;
+          if (ke > e1) s.pl[tid] = acc;
+        }
+        if (ke >= e1) break;
+        do { ++k; } while (s.cstart[k + 1] == s.cstart[k]);
       }
-      rbk_combine(s, has, run, s.est);
-    }
-    // ---- rho_k (Eq. 11 folded): GC rho = hS/EstRaw ; paper-literal sigma = hS*EstRaw ----
-    {
-      const double e = s.est[tid];
-      s.rho[tid] = form == 0 ? (e > 0.0 ? s.hSd[tid] / e : 0.0) : s.hSd[tid] * e;
     }
     __syncthreads();
-    // ---- R-pass: A_a over row-major cells (Eq. 13) ----
     {
-      Runs run;
-      const bool has = r0 < r1;
-      if (has) {
-        int a = r0 / nL, c = r0 - a * nL;
-        int ia = s.listR[a];
-        for (int e = r0; e < r1; ++e) {
-          const int k = idx0(ia, s.listL[c]);
-          const double v = form == 0 ? s.hL[c] * s.hL[c] * s.rho[k] : s.rho[k];
-          if (e == r0) run.begin(a, v); else run.step(a, v, s.rowsum);
-          if (++c == nL) {
-            c = 0;
-            ++a;
-            if (a < nR) ia = s.listR[a];
-          }
-        }
+      const int k = tid, ks = s.cstart[k], ke = s.cstart[k + 1];
+      if (ks < ke && spans(ks, ke, S)) {
+        const double e = span_sum(s, ks, ke, S);
+        s.est[k] = e;
+        s.rho[k] = form == 0 ? (e > 0.0 ? s.hSd[k] / e : 0.0) : s.hSd[k] * e;
       }
-      rbk_combine(s, has, run, s.rowsum);
-    }
-    // ---- Eq. 13 finalisation per row ----
-    {
-      double v = 0.0;
-      if (tid < nR) {
-        const double hr = s.hR[tid];
-        const double num = form == 0 ? hr * s.rowsum[tid] / N : s.rowsum[tid] / (N * hr);
-        v = (num + P.beta * s.hGc[tid]) / (SL2 / N2 + P.beta);
-        v = v > 0.0 ? v : 0.0;
-        s.hR1[tid] = v;
-        s.wgt[tid] = form == 0 ? v * hr : v / hr;
-      }
-      slot_put(s, R_SR1, v);
-      slot_put(s, R_SR2, v * v);
     }
     __syncthreads();
+
+    // ======== R-pass (Eq. 13): A_a over row-major cells ========
+    double sr1 = 0.0, sr2 = 0.0;
+    const double denR = SL2 / N2 + P.beta;
+    auto finR = [&](int a, double A) {
+      const double hr = s.hR[a];
+      const double num = form == 0 ? hr * A / N : A / (N * hr);
+      double v = (num + P.beta * s.hGc[a]) / denR;
+      v = v > 0.0 ? v : 0.0;
+      s.hR1[a] = v;
+      s.wgt[a] = form == 0 ? v * hr : v / hr;
+      sr1 += v;
+      sr2 += v * v;
+    };
+    if (has) {
+      int a = astart;
+      for (;;) {
+        const int as = a * nL, ae = as + nL;
+        const int lo = max(as, e0), hi = min(ae, e1);
+        const int ia = s.listR[a];
+        double acc = 0.0;
+        for (int e = lo; e < hi; ++e) {
+          const int c = e - as;
+          const double r = s.rho[idx0(ia, s.listL[c])];
+          acc += form == 0 ? s.hL2[c] * r : r;
+        }
+        if (as >= e0 && ae <= e1) {
+          finR(a, acc);
+        } else {
+          if (as < e0) s.pf[tid] = acc;
+          if (ae > e1) s.pl[tid] = acc;
+        }
+        if (ae >= e1) break;
+        ++a;
+      }
+    }
+    __syncthreads();
+    if (tid < nR) {
+      const int as = tid * nL, ae = as + nL;
+      if (spans(as, ae, S)) finR(tid, span_sum(s, as, ae, S));
+    }
+    slot_put(s, R_SR1, sr1);
+    slot_put(s, R_SR2, sr2);
+    __syncthreads();
+
+    // ======== L-pass (Eq. 12, frozen K): B_c over column-major cells ========
     const double SR2 = slot_sum(s, R_SR2);
-    // ---- L-pass: B_c over column-major cells (Eq. 12, frozen K) ----
-    {
-      Runs run;
-      const bool has = r0 < r1;
-      if (has) {
-        int c = r0 / nR, a = r0 - c * nR;
-        int jc = s.listL[c];
-        for (int e = r0; e < r1; ++e) {
-          const int k = idx0(s.listR[a], jc);
-          const double v = s.wgt[a] * s.rho[k];
-          if (e == r0) run.begin(c, v); else run.step(c, v, s.colsum);
-          if (++a == nR) {
-            a = 0;
-            ++c;
-            if (c < nL) jc = s.listL[c];
-          }
+    const double denL = SR2 / N2 + P.alpha;
+    double sl1 = 0.0;
+    auto finL = [&](int c, double Bv) {
+      const double hl = s.hL[c];
+      const double num = form == 0 ? hl * Bv / N : Bv / (N * hl);
+      double u = (num + P.alpha * s.hSc[c]) / denL;
+      u = u > 0.0 ? u : 0.0;
+      s.hL1[c] = u;
+      sl1 += u;
+    };
+    if (has) {
+      int c = cstart0;
+      for (;;) {
+        const int cs = c * nR, ce = cs + nR;
+        const int lo = max(cs, e0), hi = min(ce, e1);
+        const int jc = s.listL[c];
+        double acc = 0.0;
+        for (int e = lo; e < hi; ++e) {
+          const int a = e - cs;
+          acc += s.wgt[a] * s.rho[idx0(s.listR[a], jc)];
         }
+        if (cs >= e0 && ce <= e1) {
+          finL(c, acc);
+        } else {
+          if (cs < e0) s.pf[tid] = acc;
+          if (ce > e1) s.pl[tid] = acc;
+        }
+        if (ce >= e1) break;
+        ++c;
       }
-      rbk_combine(s, has, run, s.colsum);
-    }
-    // ---- Eq. 12 finalisation per column ----
-    {
-      double u = 0.0;
-      if (tid < nL) {
-        const double hl = s.hL[tid];
-        const double num = form == 0 ? hl * s.colsum[tid] / N : s.colsum[tid] / (N * hl);
-        u = (num + P.alpha * s.hSc[tid]) / (SR2 / N2 + P.alpha);
-        u = u > 0.0 ? u : 0.0;
-        s.hL1[tid] = u;
-      }
-      slot_put(s, R_SL1, u);
     }
     __syncthreads();
-    // ---- Eqs. 15, 14: renormalise; stop test (R11); Eq. 11 refresh is implicit ----
+    if (tid < nL) {
+      const int cs = tid * nR, ce = cs + nR;
+      if (spans(cs, ce, S)) finL(tid, span_sum(s, cs, ce, S));
+    }
+    slot_put(s, R_SL1, sl1);
+    __syncthreads();
+
+    // ======== Eqs. 15, 14: renormalise; stop test (R11); Eq. 11 refresh is implicit ========
     {
       const double SR1 = slot_sum(s, R_SR1), SL1 = slot_sum(s, R_SL1);
-      double dr = 0.0, dl = 0.0, l2 = 0.0;
+      double dr = 0.0, dl = 0.0, q = 0.0;
       if (tid < nR) {
         const double n = N * s.hR1[tid] / SR1;
         dr = (n - s.hR[tid]) * (n - s.hR[tid]);
@@ -543,12 +504,12 @@ __global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
         const double n = N * s.hL1[tid] / SL1;
         dl = (n - s.hL[tid]) * (n - s.hL[tid]);
         s.hL[tid] = n;
-        l2 = n * n;
+        s.hL2[tid] = n * n;
+        q = n * n;
       }
-      s.est[tid] = 0.0;
       slot_put(s, R_DR, dr);
       slot_put(s, R_DL, dl);
-      slot_put(s, R_SL2, l2);
+      slot_put(s, R_SL2, q);
     }
     __syncthreads();
     ++t;
@@ -559,22 +520,13 @@ __global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
   }
 
   // ---- outputs hL, hR (dense, zero off support) ----
-  {
-    const int pl = s.posL[tid];
-    const bool inL = s.hSi[tid] != 0u;
-    if (args.hL) args.hL[b * kLevels + tid] = inL ? s.hL[pl] : 0.0;
-    if (args.hR) {
-      // position of tid in listR: scan again (cheap)
-      args.hR[b * kLevels + tid] = 0.0;
-    }
-  }
-  __syncthreads();
-  if (args.hR && tid < nR) args.hR[b * kLevels + s.listR[tid]] = s.hR[tid];
+  if (args.hL) args.hL[b * kLevels + tid] = fL ? s.hL[pL] : 0.0;
+  if (args.hR) args.hR[b * kLevels + tid] = fR ? s.hR[pR] : 0.0;
   if (args.iters && tid == 0) args.iters[b] = t;
 
   // ---- Eq. 20 with index_1 (Eqs. 17-19): warp per row, segmented by k, warp-private sums ----
-  double* pj = s.hR1;               // p_j = b_j^(1/gamma)   (Eq. 17)
-  double* Twarp = reinterpret_cast<double*>(cells);  // 8 x 256 doubles = 16 KB (cells dead)
+  double* pj = s.hR1;                                   // p_j = b_j^(1/gamma)   (Eq. 17)
+  double* Twarp = reinterpret_cast<double*>(cells);     // 8 x 256 doubles = 16 KB (cells dead)
   {
     const double bj = s.bk[tid];
     pj[tid] = (P.gamma == 1.0) ? bj : pow(bj, 1.0 / P.gamma);
@@ -603,7 +555,7 @@ __global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
     }
   }
   __syncthreads();
-  double* Tt = s.rowsum;  // dense target
+  double* Tt = s.est;  // dense target
   {
     double acc = 0.0;
     for (int w = 0; w < NW; ++w) acc += Twarp[w * kLevels + tid];
@@ -612,7 +564,7 @@ __global__ void __launch_bounds__(T, 1) k_solve(SolveArgs args) {
   }
   __syncthreads();
   if (args.lut || args.status)
-    cdf_lut(s.hSi, Tt, s.colsum, s.est, s.rho, wscr, args.lut ? args.lut + b * kLevels : nullptr,
+    cdf_lut(s.hSi, Tt, s.hL1, s.rho, s.wgt, wscr, args.lut ? args.lut + b * kLevels : nullptr,
             args.status ? args.status + b : nullptr);
 }
 
@@ -638,7 +590,8 @@ __global__ void __launch_bounds__(T) k_match(const uint32_t* hist_s, const doubl
 
 }  // namespace
 
-size_t solve_smem_bytes() { return sizeof(Sm) + (size_t)kMaxCells * sizeof(uint16_t); }
+size_t solve_smem_bytes() { return sizeof(Sm) + (size_t)kSmemCells * sizeof(uint16_t); }
+size_t solve_cells_ws_bytes(int64_t B) { return (size_t)B * kMaxCells * sizeof(uint16_t); }
 
 cudaError_t launch_solve(const SolveArgs& a, int64_t B, cudaStream_t st) {
   static bool attr = false;

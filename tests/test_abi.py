@@ -87,9 +87,25 @@ def test_umulhi_magic_exhaustive():
     for V in range(1, 256):
         M = np.uint64((1 << 32) // (2 * V) + 1)
         assert np.array_equal((n * M) >> np.uint64(32), n // np.uint64(2 * V)), V
-    # V == 0 entry: umulhi(L + 1, 2^32 - 1) == L
+
+
+def test_apply_entry_formula_exhaustive():
+    """k_apply's per-channel formula, emulated in uint64: out = umulhi(c*e + V, M[V]) + (e >> 16)
+    with e = 2 LUT[V] (V >= 1) or LUT[0] << 16 (V = 0), M[V] = floor(2^32/2V) + 1 (M[0] = 0),
+    against floor((2 c V' + V) / 2V) (V = 0 -> V') for every V, every c <= V and every V'."""
     L = np.arange(256, dtype=np.uint64)
-    assert np.array_equal(((L + 1) * np.uint64(0xFFFFFFFF)) >> np.uint64(32), L)
+    for V in range(0, 256):
+        c = np.arange(0, V + 1, dtype=np.uint64)[:, None]
+        if V == 0:
+            e = L << np.uint64(16)
+            M = np.uint64(0)
+        else:
+            e = np.uint64(2) * L
+            M = np.uint64((1 << 32) // (2 * V) + 1)
+        n = (c * e[None, :] + np.uint64(V)) & np.uint64(0xFFFFFFFF)
+        out = ((n * M) >> np.uint64(32)) + (e[None, :] >> np.uint64(16))
+        ref = np.broadcast_to(L[None, :], out.shape) if V == 0 else (2 * c * L[None, :] + V) // (2 * V)
+        assert np.array_equal(out, ref), V
 
 
 def test_maxnorm_integer_formula_vs_rational():
