@@ -3,8 +3,10 @@
 // Every entry point validates synchronously and enqueues nothing on error.  No exception
 // or exit() crosses the boundary.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <new>
 #include <vector>
 
@@ -15,6 +17,18 @@ struct hr_ctx {
   int num_sms = 148;
   int l2_bytes = 0;
   char last_error[512] = {0};
+  // index_1 tables of Eqs. 17-19, one per gamma (64 KB each, built on first use, stream-ordered)
+  static constexpr int kTab = 8;
+  uint8_t* idx1_tab[kTab] = {};
+  double idx1_gamma[kTab] = {};
+  int idx1_next = 0;
+  // execution policy of hr_enhance (defaults chosen from B200 measurements; HR_* env overrides)
+  int chunks = 1;         // >1: fork/join pipeline over image chunks (hist | solve | apply streams)
+  int hist_cpsm = 2;      // k_hist CTAs per SM
+  int apply_cpsm = 2;     // k_apply CTAs per SM
+  int warp_solver = 0;    // 1: k_solve_warp for nR <= 32, k_solve for the rest; 0: k_solve only
+  cudaStream_t sH = nullptr, sS = nullptr, sA = nullptr;
+  std::vector<cudaEvent_t> pev;  // pipeline events
   // stage timing (hr_profile_*)
   bool prof = false;
   int prof_used = 0;
@@ -29,7 +43,7 @@ using hr::kLevels;
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WsLayout {
-  size_t hist_s, graw, lut, iters, cells, total;
+  size_t hist_s, graw, lut, iters, target, deferred, cells, total;
 };
 
 WsLayout ws_layout(int64_t B) {
@@ -42,6 +56,10 @@ WsLayout ws_layout(int64_t B) {
   L.lut = o;
   o = align_up(o + (size_t)B * kLevels);
   L.iters = o;
+  o = align_up(o + (size_t)B * sizeof(int32_t));
+  L.target = o;
+  o = align_up(o + (size_t)B * kLevels * sizeof(double));
+  L.deferred = o;
   o = align_up(o + (size_t)B * sizeof(int32_t));
   L.cells = o;
   o = align_up(o + hr::solve_cells_ws_bytes(B));
@@ -92,8 +110,26 @@ hr_status activate(hr_ctx* c) {
   return HR_OK;
 }
 
-int hist_grid(const hr_ctx* c) { return 2 * c->num_sms; }
-int apply_grid(const hr_ctx* c) { return c->num_sms; }  // launch_apply sizes its own grid
+int hist_grid(const hr_ctx* c) { return c->hist_cpsm * c->num_sms; }
+
+// index_1 table for gamma, building it on `st` when it is not cached (round-robin over kTab)
+cudaError_t idx1_table(hr_ctx* c, double gamma, cudaStream_t st, const uint8_t** out) {
+  for (int i = 0; i < hr_ctx::kTab; ++i)
+    if (c->idx1_tab[i] && c->idx1_gamma[i] == gamma) {
+      *out = c->idx1_tab[i];
+      return cudaSuccess;
+    }
+  const int i = c->idx1_next;
+  c->idx1_next = (i + 1) % hr_ctx::kTab;
+  if (!c->idx1_tab[i]) {
+    cudaError_t e = cudaMalloc(&c->idx1_tab[i], 256 * 256);
+    if (e != cudaSuccess) return e;
+  }
+  c->idx1_gamma[i] = gamma;
+  *out = c->idx1_tab[i];
+  return hr::launch_idx1_table(gamma, c->idx1_tab[i], st);
+}
+int apply_grid(const hr_ctx* c) { return c->apply_cpsm * c->num_sms; }
 
 }  // namespace
 
@@ -131,6 +167,10 @@ hr_status hr_create(hr_ctx** out, int device) {
     delete c;
     return HR_ECUDA;
   }
+  if (const char* v = getenv("HR_CHUNKS")) c->chunks = atoi(v) > 0 ? atoi(v) : 1;
+  if (const char* v = getenv("HR_HIST_CPSM")) c->hist_cpsm = atoi(v) > 0 ? atoi(v) : 2;
+  if (const char* v = getenv("HR_APPLY_CPSM")) c->apply_cpsm = atoi(v) > 0 ? atoi(v) : 2;
+  if (const char* v = getenv("HR_WARP_SOLVER")) c->warp_solver = atoi(v) != 0;
   *out = c;
   return HR_OK;
 }
@@ -138,6 +178,12 @@ hr_status hr_create(hr_ctx** out, int device) {
 hr_status hr_destroy(hr_ctx* c) {
   if (c) {
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->pev) cudaEventDestroy(e);
+    if (c->sH) cudaStreamDestroy(c->sH);
+    if (c->sS) cudaStreamDestroy(c->sS);
+    if (c->sA) cudaStreamDestroy(c->sA);
+    for (int i = 0; i < hr_ctx::kTab; ++i)
+      if (c->idx1_tab[i]) cudaFree(c->idx1_tab[i]);
   }
   delete c;
   return HR_OK;
@@ -222,7 +268,12 @@ hr_status hr_solve(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, in
   if (s) return s;
   if ((s = activate(c))) return s;
   hr::SolveArgs a{};
-  a.cells_ws = reinterpret_cast<uint16_t*>((char*)ws + ws_layout(B).cells);
+  a.cells_ws = reinterpret_cast<unsigned char*>((char*)ws + ws_layout(B).cells);
+  {
+    cudaError_t e = idx1_table(c, p->gamma, (cudaStream_t)stream, &a.idx1_tab);
+    if (e != cudaSuccess) return cuda_err(c, e, "hr_solve (index_1 table)");
+  }
+  int32_t* deferred = reinterpret_cast<int32_t*>((char*)ws + ws_layout(B).deferred);
   a.hist_s = hist_s;
   a.hist_g = hist_g;
   a.graw = nullptr;
@@ -234,7 +285,13 @@ hr_status hr_solve(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, in
   a.iters = iters;
   a.lut = nullptr;
   a.status = nullptr;
-  return cuda_err(c, hr::launch_solve(a, B, (cudaStream_t)stream), "hr_solve");
+  cudaError_t e = cudaSuccess;
+  if (c->warp_solver) {
+    e = hr::launch_solve_warp(a, B, deferred, (cudaStream_t)stream);
+    a.only_deferred = deferred;
+  }
+  if (e == cudaSuccess) e = hr::launch_solve(a, B, (cudaStream_t)stream);
+  return cuda_err(c, e, "hr_solve");
 }
 
 hr_status hr_match(hr_ctx* c, const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,
@@ -285,26 +342,83 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   uint32_t* hs = hist_s_dbg ? hist_s_dbg : reinterpret_cast<uint32_t*>((char*)ws + L.hist_s);
   uint32_t* graw = reinterpret_cast<uint32_t*>((char*)ws + L.graw);
   uint8_t* lut = lut_dbg ? lut_dbg : reinterpret_cast<uint8_t*>((char*)ws + L.lut);
-  cudaError_t e = mark(0);
-  if (e == cudaSuccess) e = cudaMemsetAsync(hs, 0, (size_t)B * kLevels * sizeof(uint32_t), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(graw, 0, (size_t)B * kGradSlots * sizeof(uint32_t), st);
-  if (e == cudaSuccess) e = hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st);
-  if (e == cudaSuccess) e = mark(1);
-  if (e == cudaSuccess) {
+  double* target = reinterpret_cast<double*>((char*)ws + L.target);
+  int32_t* deferred = reinterpret_cast<int32_t*>((char*)ws + L.deferred);
+  unsigned char* cells = reinterpret_cast<unsigned char*>((char*)ws + L.cells);
+  const uint8_t* tab = nullptr;
+  cudaError_t e = idx1_table(c, p->gamma, st, &tab);
+  const size_t img = (size_t)H * W * 3;
+  // one chunk of images [b0, b0 + nb): histograms | solve + LUT | apply, each on its stream
+  auto hist_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
+    cudaError_t r = cudaMemsetAsync(hs + b0 * kLevels, 0, (size_t)nb * kLevels * sizeof(uint32_t), s);
+    if (r == cudaSuccess) r = cudaMemsetAsync(graw + b0 * kGradSlots, 0, (size_t)nb * kGradSlots * sizeof(uint32_t), s);
+    if (r == cudaSuccess) r = hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, hist_grid(c), s);
+    return r;
+  };
+  auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
     hr::SolveArgs a{};
-    a.hist_s = hs;
+    a.idx1_tab = tab;
+    a.hist_s = hs + b0 * kLevels;
     a.hist_g = nullptr;
-    a.graw = graw;
+    a.graw = graw + b0 * kGradSlots;
     a.grad_norm = p->grad_norm;
     a.p = *p;
-    a.iters = iters_dbg;
-    a.lut = lut;
-    a.cells_ws = reinterpret_cast<uint16_t*>((char*)ws + L.cells);
-    e = hr::launch_solve(a, B, st);
+    a.iters = iters_dbg ? iters_dbg + b0 : nullptr;
+    a.target = target + b0 * kLevels;
+    a.cells_ws = cells + (size_t)b0 * (hr::solve_cells_ws_bytes(1));
+    cudaError_t r = cudaSuccess;
+    if (c->warp_solver) {
+      r = hr::launch_solve_warp(a, nb, deferred + b0, s);
+      a.only_deferred = deferred + b0;
+    }
+    if (r == cudaSuccess) r = hr::launch_solve(a, nb, s);
+    if (r == cudaSuccess) r = hr::launch_match(a.hist_s, a.target, nb, lut + b0 * kLevels, nullptr, s);
+    return r;
+  };
+  auto apply_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
+    return hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s);
+  };
+  const int K = (int)std::min<int64_t>(c->chunks, B);
+  if (K <= 1 || ev) {  // serial on the caller's stream (also the stage-timed path)
+    if (e == cudaSuccess) e = mark(0);
+    if (e == cudaSuccess) e = hist_chunk(0, B, st);
+    if (e == cudaSuccess) e = mark(1);
+    if (e == cudaSuccess) e = solve_chunk(0, B, st);
+    if (e == cudaSuccess) e = mark(2);
+    if (e == cudaSuccess) e = apply_chunk(0, B, st);
+    if (e == cudaSuccess) e = mark(3);
+    return cuda_err(c, e, "hr_enhance");
   }
-  if (e == cudaSuccess) e = mark(2);
-  if (e == cudaSuccess) e = hr::launch_apply(in, lut, B, H, W, out, apply_grid(c), st);
-  if (e == cudaSuccess) e = mark(3);
+  // fork/join pipeline: solve(c) overlaps hist(c+1) and apply(c-1)
+  if (!c->sH) {
+    for (cudaStream_t* q : {&c->sH, &c->sS, &c->sA})
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(q, cudaStreamNonBlocking);
+  }
+  while (e == cudaSuccess && (int)c->pev.size() < 2 * K + 4) {
+    cudaEvent_t x;
+    e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    if (e == cudaSuccess) c->pev.push_back(x);
+  }
+  cudaEvent_t* E = c->pev.data();  // [0] fork, [1..3] joins, [4..4+K) hist done, [4+K..4+2K) solve done
+  if (e == cudaSuccess) e = cudaEventRecord(E[0], st);
+  for (cudaStream_t q : {c->sH, c->sS, c->sA})
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(q, E[0], 0);
+  for (int k = 0; k < K && e == cudaSuccess; ++k) {
+    const int64_t b0 = B * k / K, nb = B * (k + 1) / K - b0;
+    e = hist_chunk(b0, nb, c->sH);
+    if (e == cudaSuccess) e = cudaEventRecord(E[4 + k], c->sH);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->sS, E[4 + k], 0);
+    if (e == cudaSuccess) e = solve_chunk(b0, nb, c->sS);
+    if (e == cudaSuccess) e = cudaEventRecord(E[4 + K + k], c->sS);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->sA, E[4 + K + k], 0);
+    if (e == cudaSuccess) e = apply_chunk(b0, nb, c->sA);
+  }
+  int j = 1;
+  for (cudaStream_t q : {c->sH, c->sS, c->sA}) {
+    if (e == cudaSuccess) e = cudaEventRecord(E[j], q);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, E[j], 0);
+    ++j;
+  }
   return cuda_err(c, e, "hr_enhance");
 }
 

@@ -45,8 +45,13 @@ struct SolveArgs {
   int32_t* iters;           // [B] nullable
   uint8_t* lut;             // [B][256] nullable (fused CDF + LUT tail)
   int32_t* status;          // [B] nullable
-  uint16_t* cells_ws;       // [B][65536] cell lists of images whose supports exceed shared memory
+  unsigned char* cells_ws;  // [B][kArenaGlobal] run arenas of images whose runs exceed shared memory
+  const uint8_t* idx1_tab;  // [256][256] index_1(i, j) for params.gamma (launch_idx1_table)
+  const int32_t* only_deferred;  // k_solve: when set, images with only_deferred[b] == 0 are skipped
 };
+// warp-per-image solver for nR <= 32; flags the other images in deferred[b] (then run k_solve)
+cudaError_t launch_solve_warp(const SolveArgs& a, int64_t B, int32_t* deferred, cudaStream_t st);
+cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st);
 cudaError_t launch_solve(const SolveArgs& a, int64_t B, cudaStream_t st);
 size_t solve_smem_bytes();
 size_t solve_cells_ws_bytes(int64_t B);
@@ -55,6 +60,6 @@ cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B
                          int32_t* status, cudaStream_t st);
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
-                         uint8_t* out, int num_sms, cudaStream_t st);
+                         uint8_t* out, int grid_ctas, cudaStream_t st);
 
 }  // namespace hr

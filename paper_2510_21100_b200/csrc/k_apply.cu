@@ -259,7 +259,7 @@ k_apply_scalar(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, 
 }  // namespace
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
-                         int num_sms, cudaStream_t st) {
+                         int grid_ctas, cudaStream_t st) {
   const int64_t HW = (int64_t)H * W;
   const bool tma = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                    (HW % 16 == 0) && B * ((HW + kChunkPx - 1) / kChunkPx) < (1LL << 31);
@@ -272,12 +272,12 @@ cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32
       attr = true;
     }
     const int64_t chunks = B * ((HW + kChunkPx - 1) / kChunkPx);
-    int64_t grid = 2LL * num_sms;
+    int64_t grid = grid_ctas;
     if (grid > (chunks + kWarps - 1) / kWarps) grid = (chunks + kWarps - 1) / kWarps;
     if (grid < 1) grid = 1;
     k_apply_tma<<<(unsigned)grid, kApplyThreads, sizeof(ApplySmem), st>>>(in, lut, B, HW, out);
   } else {
-    int64_t grid = 8LL * num_sms;
+    int64_t grid = 4LL * grid_ctas;
     const int64_t P = B * HW;
     if (grid > (P + kApplyThreads - 1) / kApplyThreads) grid = (P + kApplyThreads - 1) / kApplyThreads;
     if (grid < 1) grid = 1;

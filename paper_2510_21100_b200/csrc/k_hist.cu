@@ -139,6 +139,7 @@ k_hist(const uint8_t* __restrict__ rgb, int64_t B, int H, int W, uint32_t* __res
 #pragma unroll
         for (int q = 0; q < G; ++q) Vp[q] = Dp[q] = 0u;
 
+#pragma unroll 2
         for (int it = 0; it <= RPG; ++it) {
           const int y = ya + it;
           const bool inBand = active && y < yb;
