@@ -131,7 +131,12 @@ hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_de
                    int32_t H, int32_t W, uint8_t* rgb_out_dev, void* stream);
 
 /* Steps (1)-(4) for the whole batch ("matching its histogram with the one provided by
-   HistRetinex"), enqueued as one CUDA graph per (shape, params, pointers) on `stream`.
+   HistRetinex") on `stream`.  Execution policy (hr_set_policy): for B >= fused_min_b (default
+   0 = off) with 16-byte aligned buffers and H*W % 16 == 0, ONE persistent kernel runs the
+   histograms, each image's solve + LUT as soon as its histograms are complete, and the
+   apply (solves overlap the streaming passes); otherwise the histogram, solve + LUT and
+   apply kernels run in order (or as a chunk pipeline when chunks > 1).  Every policy gives
+   bit-identical outputs.  While stage profiling is enabled the separate kernels are used.
    Optional debug outputs (device, nullable): hist_s [B][256], lut [B][256], iters [B].
    rgb_out must not alias rgb_in.  Workspace: hr_workspace_bytes(B,H,W), device. */
 hr_status hr_enhance(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H, int32_t W,
@@ -143,13 +148,31 @@ hr_status hr_enhance_debug(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, in
                            void* stream);
 
 /* Stage timing (measurement only).  While enabled, every hr_enhance records four CUDA
-   events on its stream: before the histogram kernel, after it, after the solver, after the
-   apply kernel.  hr_profile_collect waits for the recorded events, returns the summed
-   milliseconds of the three stages (stage_ms[0] histogram incl. its memsets, [1] solve +
-   LUT, [2] apply) over the *steps calls since the last collect, and resets the counters.
-   At most 4096 calls are kept between collects (HR_EINVAL beyond). */
+   events on its stream.  Separate-kernel path: before the histogram kernel, after it,
+   after the solver + LUT, after the apply kernel -> stage_ms[0] histogram incl. its
+   memsets, [1] solve + LUT, [2] apply.  Fused path: before the accumulator memset, before
+   the fused kernel, after it (twice) -> stage_ms[0] memset, [1] the fused kernel, [2] 0.
+   hr_profile_collect waits for the recorded events, returns the summed milliseconds over
+   the *steps calls since the last collect, and resets the counters.  At most 4096 calls
+   are kept between collects (HR_EINVAL beyond). */
 hr_status hr_profile_enable(hr_ctx* ctx, int32_t on);
 hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
+
+/* Execution policy of hr_enhance (performance only: results never depend on it).  Keys:
+     "fused_min_b"  persistent fused kernel for B >= value (0: never)        default 0
+     "fused_cpsm"   fused-kernel CTAs per SM (1..2)                           default 2
+     "fused_bands"  histogram band work items per CTA (1..2^20)            default 4
+     "fused_gs"     512-pixel chunks per apply work ticket (1..2^30)         default 4
+     "chunks"       unfused path: image chunks of the stream pipeline (>= 1)  default 1
+     "hist_cpsm", "apply_cpsm"  unfused kernels' CTAs per SM (1..2)         default 2
+     "warp_solver"  unfused path: warp-per-image solver for small supports   default 0
+   The environment variables HR_<KEY upper-cased> set the initial values at hr_create.
+   Returns HR_EINVAL for an unknown key or an out-of-range value (nothing changes). */
+hr_status hr_set_policy(hr_ctx* ctx, const char* key, int64_t value);
+
+/* Number of CUDA kernels this context has launched so far (all entry points; memsets are
+   not kernels of this library and are not counted).  -1 for a NULL ctx. */
+int64_t hr_kernel_launches(const hr_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -22,7 +22,8 @@ from . import _lib
 from ._lib import HrError
 
 __all__ = ["Params", "HrError", "hr_histogram", "hr_solve", "hr_match", "hr_apply", "hr_enhance",
-           "hr_enhance_debug", "workspace_bytes", "version", "profile_enable", "profile_collect"]
+           "hr_enhance_debug", "workspace_bytes", "version", "profile_enable", "profile_collect",
+           "set_policy", "kernel_launches"]
 
 
 @dataclass
@@ -197,6 +198,20 @@ def profile_collect(device=None):
     n = ctypes.c_int32(0)
     _check(_lib.load().hr_profile_collect(ctx, ms, ctypes.byref(n)), ctx)
     return (ms[0], ms[1], ms[2]), n.value
+
+
+def set_policy(key: str, value: int, device=None) -> None:
+    """hr_set_policy: execution policy of hr_enhance on `device` (performance only; see
+    include/histretinex.h for the keys)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    ctx = _context(dev)
+    _check(_lib.load().hr_set_policy(ctx, key.encode(), int(value)), ctx)
+
+
+def kernel_launches(device=None) -> int:
+    """hr_kernel_launches: kernels launched so far through the context of `device`."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    return int(_lib.load().hr_kernel_launches(_context(dev)))
 
 
 def hr_enhance_debug(rgb: torch.Tensor, params: Params | None = None):

@@ -17,7 +17,8 @@ HR_OK, HR_EINVAL, HR_EEMPTY, HR_EDEGENERATE, HR_ECUDA, HR_EUNSUPPORTED = range(6
 EXPORTS = (
     "hr_default_params", "hr_create", "hr_destroy", "hr_status_string", "hr_last_error",
     "hr_version", "hr_workspace_bytes", "hr_histogram", "hr_solve", "hr_match", "hr_apply",
-    "hr_enhance", "hr_enhance_debug", "hr_profile_enable", "hr_profile_collect",
+    "hr_enhance", "hr_enhance_debug", "hr_profile_enable", "hr_profile_collect", "hr_set_policy",
+    "hr_kernel_launches",
 )
 
 
@@ -75,6 +76,8 @@ def load() -> ctypes.CDLL:
         "hr_enhance_debug": ([vp, vp, i64, i32, i32, P, vp, vp, vp, vp, vp, vp], i32),
         "hr_profile_enable": ([vp, i32], i32),
         "hr_profile_collect": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)], i32),
+        "hr_set_policy": ([vp, ctypes.c_char_p, i64], i32),
+        "hr_kernel_launches": ([vp], i64),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

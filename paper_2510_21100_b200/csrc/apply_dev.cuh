@@ -1,0 +1,147 @@
+// apply_dev.cuh -- device helpers of kernel (d): the exact integer colour reconstruction and
+// the TMA bulk-copy / mbarrier PTX wrappers.  Shared by k_apply (k_apply.cu) and the persistent
+// fused kernel (k_fused.cu).
+//
+// P:308 ("we utilize the histogram matching to estimate the enhanced image") and P:59
+// (S is the HSV value channel): V = max(R,G,B), V' = LUT[V]; replacing V in hexcone HSV
+// scales every channel by V'/V (reading R17), rounded half up:
+//     out_c = floor((2 c V' + V) / (2 V)),  V = 0 -> (V', V', V').
+// Exact integer form: out_c = umulhi(c * e + V, M[V]) + (e >> 16) with the per-level entry
+//     V >= 1: e = 2 LUT[V],  M = floor(2^32 / (2V)) + 1   (exact for every numerator <= 130305)
+//     V == 0: e = LUT[0] << 16 (then c = 0, the numerator is 0 and the addend gives LUT[0]),
+// i.e. one IMAD and one IMAD.HI (with addend) per channel.
+//
+// B200 design: every warp runs its own TMA bulk-copy pipeline over 512-pixel chunks
+// (1,536 B): cp.async.bulk global->smem completes on a per-stage mbarrier, the 32 lanes
+// transform their 16 pixels in place (three conflict-free 16-B LDS/STS at a 48-B lane
+// stride), and cp.async.bulk smem->global writes whole lines back -- no partial-sector
+// stores (the v1 per-thread 48-B STG pattern sent 1.4x the bytes to L2).  M lives in a
+// lane-private table (word 32v + lane: conflict-free), (A | Bv << 16) in a per-warp table
+// rebuilt when the warp's chunk changes image, so warps never synchronise with each other.
+// Chunks never straddle images; images whose pixel count is not a multiple of 16 (or
+// unaligned buffers) take the scalar fallback kernel.
+#pragma once
+#include "hr_common.cuh"
+
+namespace hr {
+namespace {
+
+constexpr int kWarps = kApplyThreads / 32;
+constexpr int kChunkPx = 512;
+constexpr int kChunkBytes = kChunkPx * 3;  // 1536
+constexpr int kStages = 5;
+constexpr int kAhead = kStages - 2;  // chunks prefetched ahead of the one being computed
+
+__device__ __forceinline__ uint32_t bx(uint32_t w, int k) { return __byte_perm(w, 0u, 0x4440u | (uint32_t)k); }
+
+__device__ __forceinline__ uint32_t magic_of(int v) {
+  return v == 0 ? 0u : (uint32_t)(0x100000000ull / (uint64_t)(2 * v)) + 1u;
+}
+__device__ __forceinline__ uint32_t ab_of(int v, uint32_t L) { return v == 0 ? (L << 16) : (2u * L); }
+
+// one pixel channel: floor((2 c V' + V) / 2V) = umulhi(c*e + V, M) + F
+__device__ __forceinline__ uint32_t chan(uint32_t c, uint32_t e, uint32_t v, uint32_t M, uint32_t F) {
+  return __umulhi(c * e + v, M) + F;
+}
+
+// 4 pixels in 3 words -> 3 words.  ab: per-warp table, mt: lane-private magic table.
+__device__ __forceinline__ void apply4(uint32_t w0, uint32_t w1, uint32_t w2, const uint32_t* __restrict__ ab,
+                                       const uint32_t* __restrict__ mt, int lane, uint32_t& o0, uint32_t& o1,
+                                       uint32_t& o2) {
+  const uint32_t r0 = bx(w0, 0), g0 = bx(w0, 1), b0 = bx(w0, 2);
+  const uint32_t r1 = bx(w0, 3), g1 = bx(w1, 0), b1 = bx(w1, 1);
+  const uint32_t r2 = bx(w1, 2), g2 = bx(w1, 3), b2 = bx(w2, 0);
+  const uint32_t r3 = bx(w2, 1), g3 = bx(w2, 2), b3 = bx(w2, 3);
+  const uint32_t v0 = __vimax3_u32(r0, g0, b0), v1 = __vimax3_u32(r1, g1, b1);
+  const uint32_t v2 = __vimax3_u32(r2, g2, b2), v3 = __vimax3_u32(r3, g3, b3);
+  const uint32_t e0 = ab[v0], e1 = ab[v1], e2 = ab[v2], e3 = ab[v3];
+  const uint32_t m0 = mt[(v0 << 5) | lane], m1 = mt[(v1 << 5) | lane];
+  const uint32_t m2 = mt[(v2 << 5) | lane], m3 = mt[(v3 << 5) | lane];
+  const uint32_t F0 = e0 >> 16, F1 = e1 >> 16, F2 = e2 >> 16, F3 = e3 >> 16;
+  const uint32_t R0 = chan(r0, e0, v0, m0, F0), G0 = chan(g0, e0, v0, m0, F0), Q0 = chan(b0, e0, v0, m0, F0);
+  const uint32_t R1 = chan(r1, e1, v1, m1, F1), G1 = chan(g1, e1, v1, m1, F1), Q1 = chan(b1, e1, v1, m1, F1);
+  const uint32_t R2 = chan(r2, e2, v2, m2, F2), G2 = chan(g2, e2, v2, m2, F2), Q2 = chan(b2, e2, v2, m2, F2);
+  const uint32_t R3 = chan(r3, e3, v3, m3, F3), G3 = chan(g3, e3, v3, m3, F3), Q3 = chan(b3, e3, v3, m3, F3);
+  o0 = __byte_perm(__byte_perm(R0, G0, 0x3340u), __byte_perm(Q0, R1, 0x3340u), 0x5410u);
+  o1 = __byte_perm(__byte_perm(G1, Q1, 0x3340u), __byte_perm(R2, G2, 0x3340u), 0x5410u);
+  o2 = __byte_perm(__byte_perm(Q2, R3, 0x3340u), __byte_perm(G3, Q3, 0x3340u), 0x5410u);
+}
+
+// ---- PTX wrappers: mbarrier + bulk async copies (sm_90+, used on sm_100a) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+struct __align__(128) ApplySmem {
+  uint8_t stage[kWarps][kStages][kChunkBytes];  // 60 KB
+  uint32_t mt[kLevels * 32];                    // 32 KB lane-private magic
+  uint32_t ab[kWarps][kLevels];                 // 8 KB per-warp (A | Bv << 16)
+  uint64_t bar[kWarps][kStages];
+};
+
+// One staged chunk (<= 512 px at p, `bytes` valid) transformed in place by the 32 lanes:
+// lane l owns pixels [16 l, 16 l + 16) -- three conflict-free 16-B LDS/STS at a 48-B stride.
+__device__ __forceinline__ void apply_chunk_smem(uint8_t* p, uint32_t bytes, const uint32_t* __restrict__ ab,
+                                                 const uint32_t* __restrict__ mt, int lane) {
+  if ((uint32_t)lane * 48u < bytes) {
+    uint4* q = reinterpret_cast<uint4*>(p + lane * 48);
+    const uint4 a = q[0], c = q[1], d = q[2];
+    uint4 x, y, z;
+    apply4(a.x, a.y, a.z, ab, mt, lane, x.x, x.y, x.z);
+    apply4(a.w, c.x, c.y, ab, mt, lane, x.w, y.x, y.y);
+    apply4(c.z, c.w, d.x, ab, mt, lane, y.z, y.w, z.x);
+    apply4(d.y, d.z, d.w, ab, mt, lane, z.y, z.z, z.w);
+    q[0] = x;
+    q[1] = y;
+    q[2] = z;
+  }
+}
+
+}  // namespace
+}  // namespace hr

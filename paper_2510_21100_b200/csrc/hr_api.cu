@@ -27,6 +27,11 @@ struct hr_ctx {
   int hist_cpsm = 2;      // k_hist CTAs per SM
   int apply_cpsm = 2;     // k_apply CTAs per SM
   int warp_solver = 0;    // 1: k_solve_warp for nR <= 32, k_solve for the rest; 0: k_solve only
+  int fused_min_b = 0;    // hr_enhance: persistent fused kernel for B >= this (0: never)
+  int fused_cpsm = 2;     // k_fused CTAs per SM
+  int fused_bands = 4;    // histogram band items per CTA (sets bands per image)
+  int fused_gs = 4;       // 512-px chunks per apply ticket
+  int64_t launches = 0;   // kernels launched through this context (hr_kernel_launches)
   cudaStream_t sH = nullptr, sS = nullptr, sA = nullptr;
   std::vector<cudaEvent_t> pev;  // pipeline events
   // stage timing (hr_profile_*)
@@ -42,8 +47,14 @@ using hr::kLevels;
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// count a successful kernel launch
+inline cudaError_t counted(hr_ctx* c, cudaError_t e) {
+  if (e == cudaSuccess) ++c->launches;
+  return e;
+}
+
 struct WsLayout {
-  size_t hist_s, graw, lut, iters, target, deferred, cells, total;
+  size_t hist_s, graw, ctl, lut, iters, target, deferred, cells, total;
 };
 
 WsLayout ws_layout(int64_t B) {
@@ -53,6 +64,8 @@ WsLayout ws_layout(int64_t B) {
   o = align_up(o + (size_t)B * kLevels * sizeof(uint32_t));
   L.graw = o;
   o = align_up(o + (size_t)B * kGradSlots * sizeof(uint32_t));
+  L.ctl = o;  // fused-kernel control block, right after graw: one memset clears all three
+  o = align_up(o + hr::fused_ctl_bytes(B));
   L.lut = o;
   o = align_up(o + (size_t)B * kLevels);
   L.iters = o;
@@ -127,7 +140,7 @@ cudaError_t idx1_table(hr_ctx* c, double gamma, cudaStream_t st, const uint8_t**
   }
   c->idx1_gamma[i] = gamma;
   *out = c->idx1_tab[i];
-  return hr::launch_idx1_table(gamma, c->idx1_tab[i], st);
+  return counted(c, hr::launch_idx1_table(gamma, c->idx1_tab[i], st));
 }
 int apply_grid(const hr_ctx* c) { return c->apply_cpsm * c->num_sms; }
 
@@ -171,6 +184,10 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_HIST_CPSM")) c->hist_cpsm = atoi(v) > 0 ? atoi(v) : 2;
   if (const char* v = getenv("HR_APPLY_CPSM")) c->apply_cpsm = atoi(v) > 0 ? atoi(v) : 2;
   if (const char* v = getenv("HR_WARP_SOLVER")) c->warp_solver = atoi(v) != 0;
+  if (const char* v = getenv("HR_FUSED_MIN_B")) c->fused_min_b = atoi(v) >= 0 ? atoi(v) : 0;
+  if (const char* v = getenv("HR_FUSED_CPSM")) c->fused_cpsm = atoi(v) > 0 ? atoi(v) : 2;
+  if (const char* v = getenv("HR_FUSED_BANDS")) c->fused_bands = atoi(v) > 0 ? atoi(v) : 4;
+  if (const char* v = getenv("HR_FUSED_GS")) c->fused_gs = atoi(v) > 0 ? atoi(v) : 4;
   *out = c;
   return HR_OK;
 }
@@ -194,6 +211,31 @@ hr_status hr_profile_enable(hr_ctx* c, int32_t on) {
   c->prof = on != 0;
   c->prof_used = 0;
   return HR_OK;
+}
+
+int64_t hr_kernel_launches(const hr_ctx* c) { return c ? c->launches : -1; }
+
+hr_status hr_set_policy(hr_ctx* c, const char* key, int64_t v) {
+  if (!c) return HR_EINVAL;
+  if (!key) return set_err(c, HR_EINVAL, "NULL key");
+  struct Knob {
+    const char* name;
+    int* field;
+    int64_t lo, hi;
+  };
+  const Knob knobs[] = {
+      {"fused_min_b", &c->fused_min_b, 0, 1 << 30}, {"fused_cpsm", &c->fused_cpsm, 1, 2},
+      {"fused_bands", &c->fused_bands, 1, 1 << 20}, {"fused_gs", &c->fused_gs, 1, 1 << 30},
+      {"chunks", &c->chunks, 1, 1 << 16},           {"hist_cpsm", &c->hist_cpsm, 1, 2},
+      {"apply_cpsm", &c->apply_cpsm, 1, 2},         {"warp_solver", &c->warp_solver, 0, 1},
+  };
+  for (const Knob& k : knobs) {
+    if (strcmp(k.name, key) != 0) continue;
+    if (v < k.lo || v > k.hi) return set_err(c, HR_EINVAL, "policy value out of range");
+    *k.field = (int)v;
+    return HR_OK;
+  }
+  return set_err(c, HR_EINVAL, "unknown policy key");
 }
 
 hr_status hr_profile_collect(hr_ctx* c, double* stage_ms, int32_t* steps) {
@@ -254,8 +296,8 @@ hr_status hr_histogram(hr_ctx* c, const uint8_t* rgb, int64_t B, int32_t H, int3
   uint32_t* graw = hist_g_raw ? hist_g_raw : reinterpret_cast<uint32_t*>((char*)ws + L.graw);
   cudaError_t e = cudaMemsetAsync(hist_s, 0, (size_t)B * kLevels * sizeof(uint32_t), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(graw, 0, (size_t)B * kGradSlots * sizeof(uint32_t), st);
-  if (e == cudaSuccess) e = hr::launch_hist(rgb, B, H, W, hist_s, graw, hist_grid(c), st);
-  if (e == cudaSuccess) e = hr::launch_remap(graw, B, grad_norm, hist_g, st);
+  if (e == cudaSuccess) e = counted(c, hr::launch_hist(rgb, B, H, W, hist_s, graw, hist_grid(c), st));
+  if (e == cudaSuccess) e = counted(c, hr::launch_remap(graw, B, grad_norm, hist_g, st));
   return cuda_err(c, e, "hr_histogram");
 }
 
@@ -287,10 +329,10 @@ hr_status hr_solve(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, in
   a.status = nullptr;
   cudaError_t e = cudaSuccess;
   if (c->warp_solver) {
-    e = hr::launch_solve_warp(a, B, deferred, (cudaStream_t)stream);
+    e = counted(c, hr::launch_solve_warp(a, B, deferred, (cudaStream_t)stream));
     a.only_deferred = deferred;
   }
-  if (e == cudaSuccess) e = hr::launch_solve(a, B, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = counted(c, hr::launch_solve(a, B, (cudaStream_t)stream));
   return cuda_err(c, e, "hr_solve");
 }
 
@@ -301,7 +343,7 @@ hr_status hr_match(hr_ctx* c, const uint32_t* hist_s, const double* target, int6
   if (B < 1 || B > (1 << 30)) return set_err(c, HR_EINVAL, "B must be >= 1");
   hr_status s = activate(c);
   if (s) return s;
-  return cuda_err(c, hr::launch_match(hist_s, target, B, lut, img_status, (cudaStream_t)stream), "hr_match");
+  return cuda_err(c, counted(c, hr::launch_match(hist_s, target, B, lut, img_status, (cudaStream_t)stream)), "hr_match");
 }
 
 hr_status hr_apply(hr_ctx* c, const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
@@ -311,7 +353,7 @@ hr_status hr_apply(hr_ctx* c, const uint8_t* in, const uint8_t* lut, int64_t B, 
   if (s) return s;
   if (!in || !lut || !out) return set_err(c, HR_EINVAL, "NULL pointer");
   if ((s = activate(c))) return s;
-  return cuda_err(c, hr::launch_apply(in, lut, B, H, W, out, apply_grid(c), (cudaStream_t)stream), "hr_apply");
+  return cuda_err(c, counted(c, hr::launch_apply(in, lut, B, H, W, out, apply_grid(c), (cudaStream_t)stream)), "hr_apply");
 }
 
 hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, const hr_params* p,
@@ -352,7 +394,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   auto hist_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
     cudaError_t r = cudaMemsetAsync(hs + b0 * kLevels, 0, (size_t)nb * kLevels * sizeof(uint32_t), s);
     if (r == cudaSuccess) r = cudaMemsetAsync(graw + b0 * kGradSlots, 0, (size_t)nb * kGradSlots * sizeof(uint32_t), s);
-    if (r == cudaSuccess) r = hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, hist_grid(c), s);
+    if (r == cudaSuccess) r = counted(c, hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, hist_grid(c), s));
     return r;
   };
   auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
@@ -368,16 +410,51 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     a.cells_ws = cells + (size_t)b0 * (hr::solve_cells_ws_bytes(1));
     cudaError_t r = cudaSuccess;
     if (c->warp_solver) {
-      r = hr::launch_solve_warp(a, nb, deferred + b0, s);
+      r = counted(c, hr::launch_solve_warp(a, nb, deferred + b0, s));
       a.only_deferred = deferred + b0;
     }
-    if (r == cudaSuccess) r = hr::launch_solve(a, nb, s);
-    if (r == cudaSuccess) r = hr::launch_match(a.hist_s, a.target, nb, lut + b0 * kLevels, nullptr, s);
+    if (r == cudaSuccess) r = counted(c, hr::launch_solve(a, nb, s));
+    if (r == cudaSuccess) r = counted(c, hr::launch_match(a.hist_s, a.target, nb, lut + b0 * kLevels, nullptr, s));
     return r;
   };
   auto apply_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
-    return hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s);
+    return counted(c, hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s));
   };
+  // persistent fused kernel: hist -> per-image solve + LUT -> apply, solves overlapped
+  if (c->fused_min_b > 0 && B >= c->fused_min_b && hr::fused_supported(in, out, B, H, W)) {
+    uint32_t* ctl = reinterpret_cast<uint32_t*>((char*)ws + L.ctl);
+    if (e == cudaSuccess && hs != reinterpret_cast<uint32_t*>((char*)ws + L.hist_s))
+      e = cudaMemsetAsync(hs, 0, (size_t)B * kLevels * sizeof(uint32_t), st);
+    const size_t z0 = hs == reinterpret_cast<uint32_t*>((char*)ws + L.hist_s) ? L.hist_s : L.graw;
+    if (e == cudaSuccess) e = mark(0);
+    if (e == cudaSuccess) e = cudaMemsetAsync((char*)ws + z0, 0, L.ctl + hr::fused_ctl_bytes(B) - z0, st);
+    if (e == cudaSuccess) e = mark(1);
+    hr::FusedArgs f{};
+    f.in = in;
+    f.out = out;
+    f.B = B;
+    f.H = H;
+    f.W = W;
+    f.hist_s = hs;
+    f.graw = graw;
+    f.ctl = ctl;
+    f.sa.hist_s = hs;
+    f.sa.graw = graw;
+    f.sa.grad_norm = p->grad_norm;
+    f.sa.p = *p;
+    f.sa.iters = iters_dbg;
+    f.sa.lut = lut;
+    f.sa.cells_ws = cells;
+    f.sa.idx1_tab = tab;
+    const int grid = c->fused_cpsm * c->num_sms;
+    const int64_t kb = (c->fused_bands * (int64_t)grid + B - 1) / B;
+    f.KB = (int32_t)std::max<int64_t>(1, std::min<int64_t>(kb, std::max(1, H / 16)));
+    f.GS = (uint32_t)c->fused_gs;
+    if (e == cudaSuccess) e = counted(c, hr::launch_fused(f, grid, st));
+    if (e == cudaSuccess) e = mark(2);
+    if (e == cudaSuccess) e = mark(3);
+    return cuda_err(c, e, "hr_enhance");
+  }
   const int K = (int)std::min<int64_t>(c->chunks, B);
   if (K <= 1 || ev) {  // serial on the caller's stream (also the stage-timed path)
     if (e == cudaSuccess) e = mark(0);

@@ -62,4 +62,24 @@ cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
                          uint8_t* out, int grid_ctas, cudaStream_t st);
 
+// Persistent fused kernel (k_fused.cu): histograms -> per-image solve + LUT -> apply.
+constexpr int kCtlHeader = 32;  // control words before done[B]
+inline size_t fused_ctl_bytes(int64_t B) { return (size_t)(kCtlHeader + 2 * B) * sizeof(uint32_t); }
+struct FusedArgs {
+  const uint8_t* in;  // [B][H][W][3]
+  uint8_t* out;       // [B][H][W][3]
+  int64_t B;
+  int32_t H, W;
+  uint32_t* hist_s;   // [B][256]  zeroed accumulators
+  uint32_t* graw;     // [B][512]  zeroed accumulators
+  uint32_t* ctl;      // [kCtlHeader + 2B] zeroed: [0] band ticket, [1] apply ticket, done[B], ready[B]
+  SolveArgs sa;       // solver view: hist_s/graw (as above), lut, params, idx1 table, cells_ws
+  int32_t KB;         // histogram bands per image
+  uint32_t cpi;       // apply chunks per image (set by launch_fused)
+  uint32_t GS;        // chunks per apply ticket
+};
+bool fused_supported(const uint8_t* in, const uint8_t* out, int64_t B, int32_t H, int32_t W);
+size_t fused_smem_bytes();
+cudaError_t launch_fused(FusedArgs a, int grid, cudaStream_t st);
+
 }  // namespace hr

@@ -74,6 +74,7 @@ def test_null_ctx_is_einval(lib):
     lib.hr_default_params(ctypes.byref(p))
     assert lib.hr_enhance(None, None, 1, 1, 1, ctypes.byref(p), None, None, None) == _lib.HR_EINVAL
     assert lib.hr_histogram(None, None, 1, 1, 1, 0, None, None, None, None, None) == _lib.HR_EINVAL
+    assert lib.hr_set_policy(None, b"fused_min_b", 2) == _lib.HR_EINVAL
     assert lib.hr_destroy(None) == 0
 
 

@@ -1,0 +1,130 @@
+"""The persistent fused kernel (csrc/k_fused.cu) against the separate-kernel path and the oracle.
+
+hr_enhance picks the fused kernel for B >= fused_min_b (hr_set_policy); the policy is
+performance-only, so every output (pixels, hist_s, LUT, iteration counts) must be
+bit-identical to the unfused kernels for every knob value, and both must match the oracle.
+Shapes cover the three hist template paths (W % 16 == 0, W % 8 == 0, scalar loads), the
+scalar column tail, H = 1 / W = 1 degenerate rows, and shapes the fused kernel rejects
+(H*W % 16 != 0 -> separate kernels).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def hr():
+    import paper_2510_21100_b200 as m
+
+    return m
+
+
+def batch(B, H, W, seed0=0):
+    return np.stack([synth.make_image(H, W, seed=seed0 + 97 * b, peak=(0.03, 0.3, 0.08)[b % 3]) for b in range(B)])
+
+
+def run(x, params=None, **policy):
+    m = hr()
+    defaults = dict(fused_min_b=2, fused_cpsm=2, fused_bands=4, fused_gs=4)
+    defaults.update(policy)
+    for k, v in defaults.items():
+        m.set_policy(k, v)
+    try:
+        out, hs, lut, it = m.hr_enhance_debug(torch.from_numpy(x).cuda(), params)
+        torch.cuda.synchronize()
+        return out.cpu().numpy(), hs.cpu().numpy(), lut.cpu().numpy(), it.cpu().numpy()
+    finally:
+        for k, v in dict(fused_min_b=0, fused_cpsm=2, fused_bands=4, fused_gs=4).items():
+            m.set_policy(k, v)
+
+
+SHAPES = [
+    (2, 4, 4),      # one band, one chunk per image
+    (3, 37, 112),   # W % 16 == 0: 16-px strips, ragged band rows
+    (4, 30, 24),    # W % 8 == 0: 8-px strips
+    (2, 16, 17),    # H*W % 16 == 0 with odd W: scalar-load strips + column tail
+    (3, 16, 1),     # W = 1: all pixels in the scalar tail
+    (2, 1, 48),     # H = 1: no dy anywhere
+    (5, 64, 48),
+    (2, 37, 101),   # H*W % 16 != 0: the fused kernel is not used (separate kernels)
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fused_equals_unfused(shape):
+    x = batch(*shape)
+    f = run(x, fused_min_b=2)
+    u = run(x, fused_min_b=0)
+    for a, b, what in zip(f, u, ("pixels", "hist_s", "lut", "iters")):
+        assert np.array_equal(a, b), f"{what} differ between fused and unfused"
+
+
+@pytest.mark.parametrize("shape", [(3, 37, 112), (4, 30, 24), (2, 16, 17)])
+def test_fused_vs_oracle(shape):
+    x = batch(*shape, seed0=11)
+    out, hs, lut, it = run(x)
+    op = oracle.Params()
+    for b in range(x.shape[0]):
+        r = oracle.enhance(x[b], op)
+        assert np.array_equal(hs[b].astype(np.uint64), r.hS)
+        assert it[b] == r.iters
+        assert np.array_equal(lut[b].astype(np.int32), r.lut)
+        assert np.array_equal(out[b], r.out)
+
+
+@pytest.mark.parametrize("knob,values", [
+    ("fused_bands", [1, 2, 64, 4096]),   # one band per image .. one row per band
+    ("fused_gs", [1, 3, 64, 100000]),    # tiny apply tickets .. one ticket for everything
+    ("fused_cpsm", [1]),
+])
+def test_fused_policy_invariance(knob, values):
+    x = batch(6, 90, 160, seed0=5)
+    ref = run(x, fused_min_b=0)
+    for v in values:
+        got = run(x, **{knob: v})
+        for a, b, what in zip(got, ref, ("pixels", "hist_s", "lut", "iters")):
+            assert np.array_equal(a, b), f"{knob}={v}: {what} differ"
+
+
+def test_fused_param_sets():
+    x = batch(3, 48, 64, seed0=21)
+    for kw in (dict(update_form=1), dict(use_epsilon=1, epsilon=1e-3), dict(grad_norm=1, beta=0.1), dict(gamma=1.0)):
+        f = run(x, hr().Params(**kw), fused_min_b=2)
+        u = run(x, hr().Params(**kw), fused_min_b=0)
+        for a, b, what in zip(f, u, ("pixels", "hist_s", "lut", "iters")):
+            assert np.array_equal(a, b), f"{kw}: {what} differ"
+
+
+def test_fused_degenerate_images_in_batch():
+    """All-black and constant images (solver's degenerate exits) next to normal ones."""
+    x = batch(4, 32, 48, seed0=3)
+    x[1] = 0
+    x[2] = 77
+    f = run(x, fused_min_b=2)
+    u = run(x, fused_min_b=0)
+    for a, b, what in zip(f, u, ("pixels", "hist_s", "lut", "iters")):
+        assert np.array_equal(a, b), f"{what} differ"
+
+
+def test_fused_repeat_and_large_batch():
+    """Back-to-back launches reuse the zeroed control block; B = 300 > the grid's CTA count."""
+    x = batch(300, 16, 32, seed0=9)
+    a = run(x)
+    b = run(x)
+    u = run(x, fused_min_b=0)
+    for p, q, r, what in zip(a, b, u, ("pixels", "hist_s", "lut", "iters")):
+        assert np.array_equal(p, q) and np.array_equal(p, r), what
+
+
+def test_set_policy_rejects_bad_keys():
+    m = hr()
+    with pytest.raises(m.HrError):
+        m.set_policy("no_such_knob", 1)
+    with pytest.raises(m.HrError):
+        m.set_policy("fused_cpsm", 3)
+    with pytest.raises(m.HrError):
+        m.set_policy("fused_gs", 0)
