@@ -126,8 +126,9 @@ def image_params(cfg: str, b: int) -> dict:
 
 
 def make_config(cfg: str, batch: int | None = None, out: np.ndarray | None = None,
-                threads: int = 8) -> np.ndarray:
-    """The [B, H, W, 3] uint8 batch of config `cfg` (optionally only the first `batch` images).
+                threads: int = 8, first: int = 0) -> np.ndarray:
+    """The [B, H, W, 3] uint8 batch of config `cfg` (optionally only `batch` images), starting
+    at image `first` of the config's seeded image sequence (a data-parallel rank's shard).
 
     `out` may be a preallocated (e.g. pinned) uint8 array of the right shape."""
     c = CONFIGS[cfg]
@@ -136,7 +137,7 @@ def make_config(cfg: str, batch: int | None = None, out: np.ndarray | None = Non
         out = np.empty((B, c.H, c.W, 3), np.uint8)
 
     def one(b):
-        out[b] = make_image(c.H, c.W, **image_params(cfg, b))
+        out[b] = make_image(c.H, c.W, **image_params(cfg, first + b))
 
     if B == 1 or threads <= 1:
         for b in range(B):
