@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = ["csrc/hr_api.cu", "csrc/k_hist.cu", "csrc/k_solve.cu", "csrc/k_solve_warp.cu", "csrc/k_apply.cu", "csrc/k_fused.cu"]
-HEADERS = ["csrc/hr_common.cuh", "../include/histretinex.h"]
+HEADERS = ["../include/histretinex.h"]  # + every csrc/*.cuh (see stale())
 LIB = os.path.join(HERE, "libhistretinex.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -24,10 +24,13 @@ def _nvcc() -> str:
 
 
 def stale() -> bool:
+    """True when the library is missing or older than any source or header it is built from."""
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(os.path.join(HERE, f)) > t for f in SOURCES + HEADERS)
+    deps = SOURCES + HEADERS + [os.path.join("csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
+                                if f.endswith((".cuh", ".h"))]
+    return any(os.path.getmtime(os.path.join(HERE, f)) > t for f in deps)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -31,6 +31,7 @@ struct hr_ctx {
   int fused_cpsm = 2;     // k_fused CTAs per SM
   int fused_bands = 4;    // histogram band items per CTA (sets bands per image)
   int fused_gs = 4;       // 512-px chunks per apply ticket
+  int solve_cpsm = 0;     // k_solve CTAs per SM: 1, 2, or 0 = auto (1 when B <= SMs)
   int64_t launches = 0;   // kernels launched through this context (hr_kernel_launches)
   cudaStream_t sH = nullptr, sS = nullptr, sA = nullptr;
   std::vector<cudaEvent_t> pev;  // pipeline events
@@ -143,6 +144,7 @@ cudaError_t idx1_table(hr_ctx* c, double gamma, cudaStream_t st, const uint8_t**
   return counted(c, hr::launch_idx1_table(gamma, c->idx1_tab[i], st));
 }
 int apply_grid(const hr_ctx* c) { return c->apply_cpsm * c->num_sms; }
+int solve_cpsm_for(const hr_ctx* c, int64_t B) { return c->solve_cpsm ? c->solve_cpsm : (B <= c->num_sms ? 1 : 2); }
 
 }  // namespace
 
@@ -188,6 +190,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_FUSED_CPSM")) c->fused_cpsm = atoi(v) > 0 ? atoi(v) : 2;
   if (const char* v = getenv("HR_FUSED_BANDS")) c->fused_bands = atoi(v) > 0 ? atoi(v) : 4;
   if (const char* v = getenv("HR_FUSED_GS")) c->fused_gs = atoi(v) > 0 ? atoi(v) : 4;
+  if (const char* v = getenv("HR_SOLVE_CPSM")) c->solve_cpsm = atoi(v) >= 0 && atoi(v) <= 2 ? atoi(v) : 0;
   *out = c;
   return HR_OK;
 }
@@ -228,6 +231,7 @@ hr_status hr_set_policy(hr_ctx* c, const char* key, int64_t v) {
       {"fused_bands", &c->fused_bands, 1, 1 << 20}, {"fused_gs", &c->fused_gs, 1, 1 << 30},
       {"chunks", &c->chunks, 1, 1 << 16},           {"hist_cpsm", &c->hist_cpsm, 1, 2},
       {"apply_cpsm", &c->apply_cpsm, 1, 2},         {"warp_solver", &c->warp_solver, 0, 1},
+      {"solve_cpsm", &c->solve_cpsm, 0, 2},
   };
   for (const Knob& k : knobs) {
     if (strcmp(k.name, key) != 0) continue;
@@ -332,7 +336,7 @@ hr_status hr_solve(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, in
     e = counted(c, hr::launch_solve_warp(a, B, deferred, (cudaStream_t)stream));
     a.only_deferred = deferred;
   }
-  if (e == cudaSuccess) e = counted(c, hr::launch_solve(a, B, (cudaStream_t)stream));
+  if (e == cudaSuccess) e = counted(c, hr::launch_solve(a, B, solve_cpsm_for(c, B), (cudaStream_t)stream));
   return cuda_err(c, e, "hr_solve");
 }
 
@@ -413,7 +417,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       r = counted(c, hr::launch_solve_warp(a, nb, deferred + b0, s));
       a.only_deferred = deferred + b0;
     }
-    if (r == cudaSuccess) r = counted(c, hr::launch_solve(a, nb, s));
+    if (r == cudaSuccess) r = counted(c, hr::launch_solve(a, nb, solve_cpsm_for(c, nb), s));
     if (r == cudaSuccess) r = counted(c, hr::launch_match(a.hist_s, a.target, nb, lut + b0 * kLevels, nullptr, s));
     return r;
   };

@@ -52,7 +52,7 @@ struct SolveArgs {
 // warp-per-image solver for nR <= 32; flags the other images in deferred[b] (then run k_solve)
 cudaError_t launch_solve_warp(const SolveArgs& a, int64_t B, int32_t* deferred, cudaStream_t st);
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st);
-cudaError_t launch_solve(const SolveArgs& a, int64_t B, cudaStream_t st);
+cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t st);
 size_t solve_smem_bytes();
 size_t solve_cells_ws_bytes(int64_t B);
 

@@ -3,6 +3,8 @@
 //
 // Standalone launches of the solver (one CTA per image), the per-gamma index_1 table, the
 // gradient remap and the CDF/LUT match.  The device body is in solve_dev.cuh.
+#include <algorithm>
+
 #include "solve_dev.cuh"
 
 namespace hr {
@@ -51,14 +53,18 @@ __global__ void __launch_bounds__(T) k_match(const uint32_t* hist_s, const doubl
 size_t solve_smem_bytes() { return sizeof(Sm) + (size_t)kArenaSmem; }
 size_t solve_cells_ws_bytes(int64_t B) { return (size_t)B * (size_t)kArenaGlobal; }
 
-cudaError_t launch_solve(const SolveArgs& a, int64_t B, cudaStream_t st) {
+// cpsm == 1: request enough shared memory that only one solver CTA fits on an SM (the CTA
+// scheduler would otherwise pack two latency-bound solves onto one SM while others idle).
+cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t st) {
+  constexpr size_t kOnePerSm = 120 * 1024;  // 2 x (120 KB + 1 KB reserved) > 228 KB per SM
   static bool attr = false;
-  const size_t smem = solve_smem_bytes();
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max(solve_smem_bytes(), kOnePerSm));
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  const size_t smem = cpsm == 1 ? std::max(solve_smem_bytes(), kOnePerSm) : solve_smem_bytes();
   k_solve<<<(unsigned)B, T, smem, st>>>(a);
   return cudaGetLastError();
 }

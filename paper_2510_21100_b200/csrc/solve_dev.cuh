@@ -40,12 +40,22 @@ namespace {
 
 constexpr int T = kSolveThreads;
 constexpr int NW = kSolveWarps;
-// run arena: rr (u32 descriptor, bin order) + rowRun (u16) + runE, runS2 (double) per run
-constexpr int kMaxRuns = 32896;              // sum_{i<256} (i + 1): bound on the runs of any image
-constexpr int kMaskBytes = kLevels * 8 * 4;  // per-bin row bitmask (8 words per bin)
-constexpr int kArenaSmem = 80 * 1024;
-constexpr int kArenaGlobal = 720 * 1024;  // descriptors + row slots + run sums (22 B per run)
-static_assert(kArenaGlobal >= 22 * kMaxRuns + 64, "global arena too small");
+// Run arena (per image): runs = maximal equal-key segments of a compacted row; pieces = runs
+// cut into at most kPiece cells (bounds the per-thread sum chains of the E1 phase).  Pieces
+// are stored in BIN order (bin, then row, then position), so a bin's pieces are contiguous:
+//   pDesc [P] u32   lo | hi << 8 | a << 16       (persistent)
+//   pVal  [P] f64   piece values                  (persistent; build scratch before that:
+//                   runDesc [RR] u32 row order k | lo << 8 | hi << 16 | a << 24, and the
+//                   bin-ordered per-run piece counts / offsets [RR] u32)
+//   s.keyStart[k] = first piece of bin k
+constexpr int kPiece = 8;
+constexpr int kMaxRuns = 32896;                        // sum_{i<256} (i + 1): runs of any image
+constexpr int kMaxPieces = kMaxRuns + 65536 / kPiece;  // P <= RR + E / kPiece
+constexpr int kMaskBytes = kLevels * 8 * 4;            // per-bin row bitmask (8 words per bin)
+constexpr int kArenaSmem = 80 * 1024;                  // keys (E bytes) + run arena + mask tail
+constexpr int kArenaGlobal = 12 * kMaxPieces + 256;  // arena when smem is short
+static_assert(8 * kMaxPieces >= 8 * kMaxRuns, "build scratch must fit under pVal");
+static_assert(kArenaSmem >= 65536 + kMaskBytes, "keys of the largest image must fit in smem");
 
 // Phase clock marks (measurement builds only: -DHR_SOLVE_PROFILE; block kProfBlock, thread 0).
 #ifdef HR_SOLVE_PROFILE
@@ -80,11 +90,9 @@ struct __align__(16) Sm {
   double bk[kLevels];                 // b_k = k/255 (R1)
   double red[kSlots][NW];
   uint32_t hSi[kLevels], hGi[kLevels];
-  int rowStart[kLevels + 1];  // run offsets per row
-  int keyStart[kLevels + 1];  // run offsets per bin (bin order)
+  int keyStart[kLevels + 1];  // piece offsets per bin (bin order)
   uint8_t listR[kLevels], listL[kLevels];
   unsigned long long nw[NW];
-  uint32_t bunion[8];  // union of the row bin sets (run_build)
 };
 
 __device__ __forceinline__ int idx0(int i, int j) {  // P:192 index(i,j) for l = 256
@@ -260,96 +268,125 @@ __device__ __forceinline__ int mask_rank(const uint32_t* m, int a) {
   return r + __popc(m[w] & ((1u << (a & 31)) - 1u));
 }
 
-// Run structure from the cached keys kc[a * nL + c] (monotone in c).  Per-bin row bitmasks:
-// bit a of mask[k*8 + a/32] is set iff row a has a run of bin k.  Each row records its key
-// set (8 words, owned by the row's thread: no atomics); the warp of rows 32w..32w+31 then
-// transposes the 256 x 32 bit matrix with one ballot per bin.  keyStart = exclusive scan of
-// the per-bin popcounts (bin-ordered run slots), rowStart = exclusive scan of the runs per
-// row.  Returns the number of runs.
-__device__ int run_build(Sm& s, int nR, int nL, const uint8_t* kc, uint32_t* mask, uint32_t* rowset, int* wscr) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid < 8) s.bunion[tid] = 0u;
-  int kmax = 0, cnt = 0;
-  if (tid < nR) {
-    uint32_t* rs = rowset + tid * 8;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) rs[u] = 0u;
-    const uint8_t* kr = kc + tid * nL;
-    int prev = -1;
-    for (int c = 0; c < nL; ++c) {
-      const int k = kr[c];
-      if (k != prev) {
-        rs[k >> 5] |= 1u << (k & 31);
-        prev = k;
-        ++cnt;
-      }
+__host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
+
+struct RunArena {
+  uint32_t* pDesc;
+  double* pVal;
+  int RR, P;
+};
+
+// Run + piece structure of the keys keys[a * nL + c] (non-decreasing in c), built in
+// parallel over cells: thread t owns cells [E t / T, E (t+1) / T).  A cell starts a run when
+// c == 0 or its key differs from the left neighbour; a block scan numbers the runs in row
+// order.  Each run sets its row's bit in the bin's mask (atomicOr: the result is order-free);
+// its bin-ordered slot = (runs of smaller bins) + rank of its row among the bin's rows.  A
+// scan of the per-slot piece counts places every piece in bin order.  Placement: after the
+// keys in shared memory when it fits (mask tail excluded), else arenaG.
+__device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* mask, unsigned char* arenaS,
+                          unsigned char* arenaG, RunArena& A, int* wscr) {
+  const int tid = threadIdx.x;
+  const int E = nR * nL;
+  for (int i = tid; i < kLevels * 8; i += T) mask[i] = 0u;
+  const int e0 = (int)((long long)E * tid / T), e1 = (int)((long long)E * (tid + 1) / T);
+  int cnt = 0;
+  {
+    int c = e0 % nL;
+    int prev = (e0 < e1 && c > 0) ? keys[e0 - 1] : -1;
+    for (int e = e0; e < e1; ++e) {
+      const int k = keys[e];
+      cnt += (c == 0 || k != prev) ? 1 : 0;
+      prev = k;
+      if (++c == nL) c = 0;
     }
-    kmax = prev;  // keys are non-decreasing along the row
   }
   int RR;
-  const int rs0 = block_scan_excl(cnt, &RR, wscr);
-  s.rowStart[tid] = rs0;
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, d));
-  if (lane == 0) wscr[w] = kmax;
-  __syncthreads();
-  for (int u = 0; u < NW; ++u) kmax = max(kmax, wscr[u]);
-  // transpose: the warp of rows 32w..32w+31 ballots each bin present in any row of the CTA
-  // (the union of the row sets, 8 words, via shared memory); all other bins get 0 words
-  {
-    const int a = w * 32 + lane;
-    uint32_t set[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) set[u] = (a < nR) ? rowset[a * 8 + u] : 0u;
-    uint32_t uni[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      uint32_t x = set[u];
-#pragma unroll
-      for (int d = 16; d >= 1; d >>= 1) x |= __shfl_xor_sync(0xffffffffu, x, d);
-      uni[u] = x;
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) atomicOr(&s.bunion[u], uni[u]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t all = s.bunion[u];
-      mask[(u * 32 + lane) * 8 + w] = 0u;  // default; bins present are overwritten below
-      __syncwarp();
-      uint32_t rem = all;
-      while (rem) {
-        const int bit = __ffs(rem) - 1;
-        rem &= rem - 1u;
-        const uint32_t m = __ballot_sync(0xffffffffu, (set[u] >> bit) & 1u);
-        if (lane == 0) mask[(u * 32 + bit) * 8 + w] = m;
+  int r = block_scan_excl(cnt, &RR, wscr);
+  const int Pmax = RR + E / kPiece;
+  const bool sm = align16(E) + align16(4 * Pmax) + 8 * Pmax <= kArenaSmem - kMaskBytes;
+  unsigned char* base = sm ? arenaS + align16(E) : arenaG;
+  A.pDesc = reinterpret_cast<uint32_t*>(base);
+  A.pVal = reinterpret_cast<double*>(base + align16(4 * Pmax));
+  A.RR = RR;
+  uint32_t* runDesc = reinterpret_cast<uint32_t*>(A.pVal);  // build scratch under pVal
+  uint32_t* slotN = runDesc + RR;                           // bin order: pieces, then offsets
+  {  // descriptors with hi provisional (fixed below)
+    int a = e0 / nL, c = e0 - a * nL;
+    int prev = (e0 < e1 && c > 0) ? keys[e0 - 1] : -1;
+    for (int e = e0; e < e1; ++e) {
+      const int k = keys[e];
+      if (c == 0 || k != prev) runDesc[r++] = (uint32_t)k | ((uint32_t)c << 8) | ((uint32_t)a << 24);
+      prev = k;
+      if (++c == nL) {
+        c = 0;
+        ++a;
       }
     }
   }
-  (void)kmax;
+  __syncthreads();
+  // hi = next run's lo - 1 in the same row (else nL - 1); bin masks
+  const int r0 = (int)((long long)RR * tid / T), r1 = (int)((long long)RR * (tid + 1) / T);
+  for (int q = r0; q < r1; ++q) {
+    const uint32_t d = runDesc[q];
+    const int a = d >> 24, k = d & 255;
+    int hi = nL - 1;
+    if (q + 1 < RR) {
+      const uint32_t dn = runDesc[q + 1];
+      if ((int)(dn >> 24) == a) hi = (int)((dn >> 8) & 255) - 1;
+    }
+    runDesc[q] = d | ((uint32_t)hi << 16);
+    atomicOr(&mask[k * 8 + (a >> 5)], 1u << (a & 31));
+  }
   __syncthreads();
   int kcount = 0;
 #pragma unroll
   for (int u = 0; u < 8; ++u) kcount += __popc(mask[tid * 8 + u]);
   int RK;
-  const int ks = block_scan_excl(kcount, &RK, wscr);
-  s.keyStart[tid] = ks;
-  if (tid == 0) {
-    s.keyStart[kLevels] = RK;
-    s.rowStart[kLevels] = RR;
+  const int kfirst = block_scan_excl(kcount, &RK, wscr);  // first run slot of bin tid
+  s.keyStart[tid] = kfirst;
+  __syncthreads();
+  for (int q = r0; q < r1; ++q) {  // piece count at the run's bin-order slot
+    const uint32_t d = runDesc[q];
+    const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
+    slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)] = (uint32_t)((hi - lo) / kPiece + 1);
   }
   __syncthreads();
-  return RR;
+  int np = 0;  // exclusive scan of the bin-ordered piece counts -> piece offsets
+  for (int q = r0; q < r1; ++q) np += (int)slotN[q];
+  int P;
+  int off = block_scan_excl(np, &P, wscr);
+  for (int q = r0; q < r1; ++q) {
+    const int n = (int)slotN[q];
+    slotN[q] = (uint32_t)off;
+    off += n;
+  }
+  A.P = P;
+  __syncthreads();
+  for (int q = r0; q < r1; ++q) {  // pieces of each run at its bin-order offset
+    const uint32_t d = runDesc[q];
+    const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
+    int p = (int)slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)];
+    for (int l = lo; l <= hi; l += kPiece, ++p)
+      A.pDesc[p] = (uint32_t)l | ((uint32_t)min(l + kPiece - 1, hi) << 8) | ((uint32_t)a << 16);
+  }
+  __syncthreads();
+  s.keyStart[tid] = kfirst < RK ? (int)slotN[kfirst] : P;  // run slots -> piece offsets
+  if (tid == 0) s.keyStart[kLevels] = P;
+  __syncthreads();
 }
 
-// slot of row a's run of bin k in the bin-ordered run array
-__device__ __forceinline__ int run_slot(const Sm& s, const uint32_t* mask, int k, int a) {
-  return s.keyStart[k] + mask_rank(mask + k * 8, a);
+// sum over bin k of its pieces (contiguous, bin order: runs in row order)
+__device__ __forceinline__ double bin_sum(const Sm& s, const RunArena& A, int k) {
+  double e0 = 0.0, e1 = 0.0;
+  int j = s.keyStart[k];
+  const int j1 = s.keyStart[k + 1];
+  for (; j + 1 < j1; j += 2) {
+    e0 += A.pVal[j];
+    e1 += A.pVal[j + 1];
+  }
+  if (j < j1) e0 += A.pVal[j];
+  return e0 + e1;
 }
-
-__host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
 
 // fast fp64 reciprocal: MUFU.RCP64H seed and two Newton steps (within ~1 ulp)
 __device__ __forceinline__ double rcp_fast(double x) {
@@ -361,22 +398,20 @@ __device__ __forceinline__ double rcp_fast(double x) {
   return fma(r, e, r);
 }
 
-// Algorithm 1 iterations over the run arena (SM: arena in shared memory).  Returns t.
-// Arena: rr (descriptors, bin order) | rowRun (slots in row order) | runE | runS2.
+// Algorithm 1 iterations over the run arena A.  Returns t.
 // Four phases per update, each closed by a barrier:
 //   E1  renormalise the raw iterates of the previous update (Eqs. 15, 14) and, one thread per
-//       run, the run sums hR_a * sum(hL) and sum(hL^2) over the run (Eqs. 6, 8)
+//       piece, hR_a * sum(hL) over the piece (Eqs. 6, 8)
 //   E2  one thread per bin: EstRaw_k over the bin's runs in row order, rho_k (Eq. 11 folded)
-//   R   one thread per row: A_a over the row's runs, Eq. 13
-//   L   one thread per column: B_c over the rows, Eq. 12 with the frozen K
-template <bool SM>
-__device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL, int RR, double N,
-                                       unsigned char* arena, int off) {
+//   R   TPR threads per row: A_a over the row's cells (cached keys kc), Eq. 13
+//   L   TPC threads per column: B_c over the rows, Eq. 12 with the frozen K
+__device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL, double N, const uint8_t* kc,
+                                       const RunArena& A) {
   const int tid = threadIdx.x;
-  const uint32_t* rr = reinterpret_cast<const uint32_t*>(arena + off);
-  const uint16_t* rowRun = reinterpret_cast<const uint16_t*>(arena + off + align16(4 * RR));
-  double* runE = reinterpret_cast<double*>(arena + off + align16(4 * RR) + align16(2 * RR));
-  double* runS2 = runE + RR;
+  // threads per row (R) / per column (L): the largest power of two with all rows / columns
+  // covered by the T threads; each group sums its cells in a fixed order (deterministic)
+  const int lgR = nR <= T / 8 ? 3 : nR <= T / 4 ? 2 : nR <= T / 2 ? 1 : 0, TPR = 1 << lgR;
+  const int lgL = nL <= T / 8 ? 3 : nL <= T / 4 ? 2 : nL <= T / 2 ? 1 : 0, TPC = 1 << lgL;
   const int form = P.update_form;
   const double invN = 1.0 / N, invN2 = invN * invN;
   double SR1 = N, SL1 = N;  // sums of the raw iterates (initially exactly N)
@@ -390,7 +425,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
   for (;;) {
     // ======== E1: renormalise (Eqs. 15, 14); run sums of hL and hL^2 (Eqs. 6, 8) ========
     {
-      const double cR = N * rcp_fast(SR1), cL = N * rcp_fast(SL1), cRL = cR * cL, cL2 = cL * cL;
+      const double cR = N * rcp_fast(SR1), cL = N * rcp_fast(SL1), cRL = cR * cL;
       double dr = 0.0, dl = 0.0, q = 0.0;
       if (tid < nR) {
         const double n = cR * s.hR1[tid];
@@ -404,25 +439,17 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         s.hL2[tid] = n * n;
         q = n * n;
       }
-      for (int r = tid; r < RR; r += T) {
-        const uint32_t d = rr[r];
-        const int lo = (d >> 8) & 255, hi = (d >> 16) & 255, ra = d >> 24;
-        double s0 = 0.0, s1 = 0.0, q0 = 0.0, q1 = 0.0;
+      for (int p = tid; p < A.P; p += T) {  // piece sums hR_a * sum(hL over the piece)
+        const uint32_t d = A.pDesc[p];
+        const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;
+        double s0 = 0.0, s1 = 0.0;
         int c = lo;
         for (; c + 1 <= hi; c += 2) {
-          const double x0 = s.hL1[c], x1 = s.hL1[c + 1];
-          s0 += x0;
-          s1 += x1;
-          q0 = fma(x0, x0, q0);
-          q1 = fma(x1, x1, q1);
+          s0 += s.hL1[c];
+          s1 += s.hL1[c + 1];
         }
-        if (c <= hi) {
-          const double x0 = s.hL1[c];
-          s0 += x0;
-          q0 = fma(x0, x0, q0);
-        }
-        runE[r] = s.hR1[ra] * (s0 + s1) * cRL;
-        runS2[r] = (q0 + q1) * cL2;
+        if (c <= hi) s0 += s.hL1[c];
+        A.pVal[p] = s.hR1[pa] * (s0 + s1) * cRL;
       }
       slot_put3(s, R_DR, dr, R_DL, dl, R_SL2, q);
     }
@@ -433,73 +460,76 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       const bool conv = P.use_epsilon && slot_sum(s, R_DR) <= eps && slot_sum(s, R_DL) <= eps;
       if (conv || t >= P.max_iter) break;
     }
-    // ======== E2: EstRaw_k over the bin's runs in row order; rho_k (Eq. 11 folded) ========
+    // ======== E2: EstRaw_k over the bin's runs (row order) and their pieces; rho_k (Eq. 11) ========
     {
-      const int k = tid, k0 = s.keyStart[k], k1 = s.keyStart[k + 1];
-      if (k0 < k1) {
-        double e0 = 0.0, e1 = 0.0;
-        int j = k0;
-        for (; j + 1 < k1; j += 2) {
-          e0 += runE[j];
-          e1 += runE[j + 1];
-        }
-        if (j < k1) e0 += runE[j];
-        const double e = e0 + e1;  // EstRaw_k (Eqs. 6, 8)
+      const int k = tid;
+      if (s.keyStart[k] < s.keyStart[k + 1]) {
+        const double e = bin_sum(s, A, k);  // EstRaw_k (Eqs. 6, 8)
         s.rho[k] = form == 0 ? (e > 0.0 ? s.hSd[k] * rcp_fast(e) : 0.0) : s.hSd[k] * e;
       }
     }
     const double invDenR = rcp_fast(slot_sum(s, R_SL2) * invN2 + P.beta);
     __syncthreads();
     PHASE(1);
-    // ======== R: Eq. 13, one thread per row walking the row's cells ========
+    // ======== R: Eq. 13, TPR threads per row walking every TPR-th cell, fixed-order reduce ========
     {
-      double v = 0.0;
-      if (tid < nR) {
-        const int ia = s.listR[tid];
-        double a0 = 0.0, a1 = 0.0;
-        int c = 0;
+      double A0 = 0.0, A1 = 0.0;
+      const int a = tid >> lgR, p = tid & (TPR - 1);
+      if (a < nR) {
+        const uint8_t* kr = kc + a * nL;
+        int c = p;
         if (form == 0) {
-          for (; c + 1 < nL; c += 2) {
-            a0 = fma(s.hL2[c], s.rho[idx0(ia, s.listL[c])], a0);
-            a1 = fma(s.hL2[c + 1], s.rho[idx0(ia, s.listL[c + 1])], a1);
+          for (; c + TPR < nL; c += 2 * TPR) {
+            A0 = fma(s.hL2[c], s.rho[kr[c]], A0);
+            A1 = fma(s.hL2[c + TPR], s.rho[kr[c + TPR]], A1);
           }
-          if (c < nL) a0 = fma(s.hL2[c], s.rho[idx0(ia, s.listL[c])], a0);
+          if (c < nL) A0 = fma(s.hL2[c], s.rho[kr[c]], A0);
         } else {
-          for (; c + 1 < nL; c += 2) {
-            a0 += s.rho[idx0(ia, s.listL[c])];
-            a1 += s.rho[idx0(ia, s.listL[c + 1])];
+          for (; c + TPR < nL; c += 2 * TPR) {
+            A0 += s.rho[kr[c]];
+            A1 += s.rho[kr[c + TPR]];
           }
-          if (c < nL) a0 += s.rho[idx0(ia, s.listL[c])];
+          if (c < nL) A0 += s.rho[kr[c]];
         }
-        const double A = a0 + a1, hr = s.hR[tid];
+      }
+      double A = A0 + A1;
+      for (int d = TPR >> 1; d >= 1; d >>= 1) A += __shfl_xor_sync(0xffffffffu, A, d);
+      double v = 0.0;
+      if (a < nR && p == 0) {
+        const double hr = s.hR[a];
         const double num = form == 0 ? hr * A * invN : A * rcp_fast(N * hr);
-        v = (num + P.beta * s.hGc[tid]) * invDenR;
+        v = (num + P.beta * s.hGc[a]) * invDenR;
         v = v > 0.0 ? v : 0.0;
-        s.hR1[tid] = v;
-        s.wgt[tid] = form == 0 ? v * hr : v * rcp_fast(hr);
+        s.hR1[a] = v;
+        s.wgt[a] = form == 0 ? v * hr : v * rcp_fast(hr);
       }
       slot_put3(s, R_SR1, v, R_SR2, v * v, -1, 0.0);
     }
     __syncthreads();
     PHASE(2);
-    // ======== L: Eq. 12 (frozen K), one thread per column over the rows ========
+    // ======== L: Eq. 12 (frozen K), TPC threads per column over every TPC-th row ========
     {
       const double invDenL = rcp_fast(slot_sum(s, R_SR2) * invN2 + P.alpha);
-      double u = 0.0;
-      if (tid < nL) {
-        const int jc = s.listL[tid];
-        double b0 = 0.0, b1 = 0.0;
-        int a = 0;
-        for (; a + 1 < nR; a += 2) {
-          b0 = fma(s.wgt[a], s.rho[idx0(s.listR[a], jc)], b0);
-          b1 = fma(s.wgt[a + 1], s.rho[idx0(s.listR[a + 1], jc)], b1);
+      double B0 = 0.0, B1 = 0.0;
+      const int c = tid >> lgL, p = tid & (TPC - 1);
+      if (c < nL) {
+        const uint8_t* kq = kc + c;
+        int a = p;
+        for (; a + TPC < nR; a += 2 * TPC) {
+          B0 = fma(s.wgt[a], s.rho[kq[a * nL]], B0);
+          B1 = fma(s.wgt[a + TPC], s.rho[kq[(a + TPC) * nL]], B1);
         }
-        if (a < nR) b0 = fma(s.wgt[a], s.rho[idx0(s.listR[a], jc)], b0);
-        const double Bv = b0 + b1, hl = s.hL[tid];
+        if (a < nR) B0 = fma(s.wgt[a], s.rho[kq[a * nL]], B0);
+      }
+      double Bv = B0 + B1;
+      for (int d = TPC >> 1; d >= 1; d >>= 1) Bv += __shfl_xor_sync(0xffffffffu, Bv, d);
+      double u = 0.0;
+      if (c < nL && p == 0) {
+        const double hl = s.hL[c];
         const double num = form == 0 ? hl * Bv * invN : Bv * rcp_fast(N * hl);
-        u = (num + P.alpha * s.hSc[tid]) * invDenL;
+        u = (num + P.alpha * s.hSc[c]) * invDenL;
         u = u > 0.0 ? u : 0.0;
-        s.hL1[tid] = u;
+        s.hL1[c] = u;
       }
       slot_put3(s, R_SL1, u, -1, 0.0, -1, 0.0);
     }
@@ -517,39 +547,6 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
   return t;
 }
 
-// Eq. 20 run values Tv (bin order) from the cached index_1 keys kc1, then the dense target.
-template <bool SM>
-__device__ __forceinline__ void target_runs(Sm& s, int nR, int nL, const uint8_t* kc1, const uint32_t* mask,
-                                            double* Tv, double invN, double* Tt) {
-  const int tid = threadIdx.x;
-  if (tid < nR) {  // every run of row a: hR_a * sum(hL over the run) at its bin-order slot
-    const double hr = s.hR[tid];
-    const uint8_t* kr = kc1 + tid * nL;
-    int prev = kr[0];
-    double acc = s.hL[0];
-    for (int c = 1; c < nL; ++c) {
-      const int k = kr[c];
-      if (k != prev) {
-        Tv[run_slot(s, mask, prev, tid)] = hr * acc;
-        prev = k;
-        acc = 0.0;
-      }
-      acc += s.hL[c];
-    }
-    Tv[run_slot(s, mask, prev, tid)] = hr * acc;
-  }
-  __syncthreads();
-  const int k = tid, k0 = s.keyStart[k], k1 = s.keyStart[k + 1];
-  double e0 = 0.0, e1 = 0.0;
-  int j = k0;
-  for (; j + 1 < k1; j += 2) {
-    e0 += Tv[j];
-    e1 += Tv[j + 1];
-  }
-  if (j < k1) e0 += Tv[j];
-  Tt[k] = (e0 + e1) * invN;
-}
-
 // One image of Algorithm 1 + Eq. 20 + the CDF/LUT tail, by all T threads of the CTA.
 // smraw: solve_smem_bytes() of shared memory; wscr: NW ints of shared scratch.  Every exit is
 // CTA-uniform.  Histograms are read through L2 (__ldcg): in the fused kernel they were
@@ -561,9 +558,8 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   PROF_MARK();
   Sm& s = *reinterpret_cast<Sm*>(smraw);
   unsigned char* arenaS = smraw + sizeof(Sm);
-  // shared arena tail: [ ... | rowset 8 KB | mask 8 KB ]
+  // shared arena: [ keys (E bytes) | run arena (when it fits) | ... | mask 8 KB ]
   uint32_t* mask = reinterpret_cast<uint32_t*>(arenaS + kArenaSmem - kMaskBytes);
-  uint32_t* rowset = reinterpret_cast<uint32_t*>(arenaS + kArenaSmem - 2 * kMaskBytes);
   const int tid = threadIdx.x;
   const hr_params& P = args.p;
   if (args.only_deferred && args.only_deferred[b] == 0) return;  // solved by k_solve_warp
@@ -625,7 +621,7 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   }
 
   // ---- runs of index(i,j) along each compacted row (fixed for all t) ----
-  // keys kc (u8 per cell, always fits: E <= 65536 <= arena - 16 KB) at the arena start
+  // keys kc (u8 per cell, always fits: E <= 65536 <= arena - mask) at the arena start
   const int E = nR * nL;
   uint8_t* kc = arenaS;
   for (int e = tid; e < E; e += T) {
@@ -633,39 +629,12 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
     kc[e] = (uint8_t)idx0(s.listR[a], s.listL[c]);
   }
   __syncthreads();
-  const int RR = run_build(s, nR, nL, kc, mask, rowset, wscr);
-  // rr | rowRun after kc, clear of the live mask; runE | runS2 may overlap the mask
-  const int rrBytes = align16(4 * RR) + align16(2 * RR);
-  const bool inSmem = align16(E) + rrBytes <= kArenaSmem - kMaskBytes &&
-                      align16(E) + rrBytes + 16 * RR <= kArenaSmem;
-  unsigned char* arena = inSmem ? arenaS : args.cells_ws + b * (int64_t)kArenaGlobal;
-  const int off = inSmem ? align16(E) : 0;
-  {
-    uint32_t* rr = reinterpret_cast<uint32_t*>(arena + off);
-    uint16_t* rowRun = reinterpret_cast<uint16_t*>(arena + off + align16(4 * RR));
-    if (tid < nR) {  // descriptor k | lo << 8 | hi << 16 | a << 24 at the run's bin-order slot
-      const uint8_t* kr = kc + tid * nL;
-      int prev = kr[0], lo = 0, i = s.rowStart[tid];
-      for (int c = 1; c < nL; ++c) {
-        const int k = kr[c];
-        if (k != prev) {
-          const int slot = run_slot(s, mask, prev, tid);
-          rr[slot] = (uint32_t)prev | ((uint32_t)lo << 8) | ((uint32_t)(c - 1) << 16) | ((uint32_t)tid << 24);
-          rowRun[i++] = (uint16_t)slot;
-          prev = k;
-          lo = c;
-        }
-      }
-      const int slot = run_slot(s, mask, prev, tid);
-      rr[slot] = (uint32_t)prev | ((uint32_t)lo << 8) | ((uint32_t)(nL - 1) << 16) | ((uint32_t)tid << 24);
-      rowRun[i] = (uint16_t)slot;
-    }
-  }
-  __syncthreads();
+  unsigned char* arenaG = args.cells_ws + b * (int64_t)kArenaGlobal;
+  RunArena A;
+  run_build(s, nR, nL, kc, mask, arenaS, arenaG, A, wscr);
   PROF_MARK();
 
-  const int t = inSmem ? iterate<true>(s, P, nR, nL, RR, N, arenaS, off)
-                       : iterate<false>(s, P, nR, nL, RR, N, arena, off);
+  const int t = iterate(s, P, nR, nL, N, kc, A);
   PROF_MARK();
 
   // ---- outputs hL, hR (dense, zero off support) ----
@@ -681,13 +650,23 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
     kc1[e] = __ldg(args.idx1_tab + s.listR[a] * kLevels + s.listL[c]);
   }
   __syncthreads();
-  const int RT = run_build(s, nR, nL, kc1, mask, rowset, wscr);
+  run_build(s, nR, nL, kc1, mask, arenaS, arenaG, A, wscr);
+  for (int p = tid; p < A.P; p += T) {  // piece values hR_a * sum(hL over the piece)
+    const uint32_t d = A.pDesc[p];
+    const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;
+    double s0 = 0.0, s1 = 0.0;
+    int c = lo;
+    for (; c + 1 <= hi; c += 2) {
+      s0 += s.hL[c];
+      s1 += s.hL[c + 1];
+    }
+    if (c <= hi) s0 += s.hL[c];
+    A.pVal[p] = s.hR[pa] * (s0 + s1);
+  }
+  __syncthreads();
   double* Tt = s.rho;  // dense target
-  if (align16(E) + 8 * RT <= kArenaSmem - kMaskBytes)
-    target_runs<true>(s, nR, nL, kc1, mask, reinterpret_cast<double*>(arenaS + align16(E)), 1.0 / N, Tt);
-  else
-    target_runs<false>(s, nR, nL, kc1, mask, reinterpret_cast<double*>(args.cells_ws + b * (int64_t)kArenaGlobal),
-                       1.0 / N, Tt);
+  Tt[tid] = s.keyStart[tid] < s.keyStart[tid + 1] ? bin_sum(s, A, tid) / N : 0.0;
+  __syncthreads();
   if (args.target) args.target[b * kLevels + tid] = Tt[tid];
   __syncthreads();
   PROF_MARK();
