@@ -152,6 +152,7 @@ hr_status hr_enhance_debug(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, in
    after the solver + LUT, after the apply kernel -> stage_ms[0] histogram incl. its
    memsets, [1] solve + LUT, [2] apply.  Fused path: before the accumulator memset, before
    the fused kernel, after it (twice) -> stage_ms[0] memset, [1] the fused kernel, [2] 0.
+   Chunk pipeline (chunks > 1): stage_ms = [0, 0, whole pipeline].
    hr_profile_collect waits for the recorded events, returns the summed milliseconds over
    the *steps calls since the last collect, and resets the counters.  At most 4096 calls
    are kept between collects (HR_EINVAL beyond). */

@@ -11,15 +11,14 @@
 //     V == 0: e = LUT[0] << 16 (then c = 0, the numerator is 0 and the addend gives LUT[0]),
 // i.e. one IMAD and one IMAD.HI (with addend) per channel.
 //
-// B200 design: every warp runs its own TMA bulk-copy pipeline over 512-pixel chunks
-// (1,536 B): cp.async.bulk global->smem completes on a per-stage mbarrier, the 32 lanes
-// transform their 16 pixels in place (three conflict-free 16-B LDS/STS at a 48-B lane
-// stride), and cp.async.bulk smem->global writes whole lines back -- no partial-sector
-// stores (the v1 per-thread 48-B STG pattern sent 1.4x the bytes to L2).  M lives in a
-// lane-private table (word 32v + lane: conflict-free), (A | Bv << 16) in a per-warp table
-// rebuilt when the warp's chunk changes image, so warps never synchronise with each other.
-// Chunks never straddle images; images whose pixel count is not a multiple of 16 (or
-// unaligned buffers) take the scalar fallback kernel.
+// B200 design: every warp runs its own TMA bulk-copy pipeline over 1024-pixel chunks
+// (3,072 B): cp.async.bulk global->smem completes on a per-stage mbarrier, the 32 lanes
+// transform the chunk in place as two 512-px sub-blocks (lane l owns 16 px of each: three
+// conflict-free 16-B LDS/STS at a 48-B lane stride), and cp.async.bulk smem->global writes
+// whole lines back -- no partial-sector stores.  Per pixel one 8-B LDS fetches (e, M) from a
+// per-warp table rebuilt when the warp's chunk changes image (M from a compile-time constant
+// table), so warps never synchronise with each other.  Chunks never straddle images; images
+// whose pixel count is not a multiple of 16 (or unaligned buffers) take the scalar kernel.
 #pragma once
 #include "hr_common.cuh"
 
@@ -27,44 +26,60 @@ namespace hr {
 namespace {
 
 constexpr int kWarps = kApplyThreads / 32;
-constexpr int kChunkPx = 512;
-constexpr int kChunkBytes = kChunkPx * 3;  // 1536
-constexpr int kStages = 5;
+constexpr int kSubPx = 512;                 // px per sub-block: lane l owns [16 l, 16 l + 16)
+constexpr int kSubBytes = kSubPx * 3;       // 1536
+constexpr int kChunkPx = 2 * kSubPx;        // px per bulk copy
+constexpr int kChunkBytes = kChunkPx * 3;   // 3072
+constexpr int kStages = 4;
 constexpr int kAhead = kStages - 2;  // chunks prefetched ahead of the one being computed
 
 __device__ __forceinline__ uint32_t bx(uint32_t w, int k) { return __byte_perm(w, 0u, 0x4440u | (uint32_t)k); }
 
-__device__ __forceinline__ uint32_t magic_of(int v) {
+__host__ __device__ constexpr uint32_t magic_of(int v) {
   return v == 0 ? 0u : (uint32_t)(0x100000000ull / (uint64_t)(2 * v)) + 1u;
 }
-__device__ __forceinline__ uint32_t ab_of(int v, uint32_t L) { return v == 0 ? (L << 16) : (2u * L); }
+__host__ __device__ constexpr uint32_t ab_of(int v, uint32_t L) { return v == 0 ? (L << 16) : (2u * L); }
+
+struct MagicTable {
+  uint32_t m[kLevels];
+};
+__host__ __device__ constexpr MagicTable make_magic() {
+  MagicTable t{};
+  for (int v = 0; v < kLevels; ++v) t.m[v] = magic_of(v);
+  return t;
+}
+__constant__ MagicTable c_magic = make_magic();  // M[v], generated at compile time
 
 // one pixel channel: floor((2 c V' + V) / 2V) = umulhi(c*e + V, M) + F
 __device__ __forceinline__ uint32_t chan(uint32_t c, uint32_t e, uint32_t v, uint32_t M, uint32_t F) {
   return __umulhi(c * e + v, M) + F;
 }
 
-// 4 pixels in 3 words -> 3 words.  ab: per-warp table, mt: lane-private magic table.
-__device__ __forceinline__ void apply4(uint32_t w0, uint32_t w1, uint32_t w2, const uint32_t* __restrict__ ab,
-                                       const uint32_t* __restrict__ mt, int lane, uint32_t& o0, uint32_t& o1,
-                                       uint32_t& o2) {
+// 4 pixels in 3 words -> 3 words.  tab: per-warp (e, M) table.
+__device__ __forceinline__ void apply4(uint32_t w0, uint32_t w1, uint32_t w2, const uint2* __restrict__ tab,
+                                       uint32_t& o0, uint32_t& o1, uint32_t& o2) {
   const uint32_t r0 = bx(w0, 0), g0 = bx(w0, 1), b0 = bx(w0, 2);
   const uint32_t r1 = bx(w0, 3), g1 = bx(w1, 0), b1 = bx(w1, 1);
   const uint32_t r2 = bx(w1, 2), g2 = bx(w1, 3), b2 = bx(w2, 0);
   const uint32_t r3 = bx(w2, 1), g3 = bx(w2, 2), b3 = bx(w2, 3);
   const uint32_t v0 = __vimax3_u32(r0, g0, b0), v1 = __vimax3_u32(r1, g1, b1);
   const uint32_t v2 = __vimax3_u32(r2, g2, b2), v3 = __vimax3_u32(r3, g3, b3);
-  const uint32_t e0 = ab[v0], e1 = ab[v1], e2 = ab[v2], e3 = ab[v3];
-  const uint32_t m0 = mt[(v0 << 5) | lane], m1 = mt[(v1 << 5) | lane];
-  const uint32_t m2 = mt[(v2 << 5) | lane], m3 = mt[(v3 << 5) | lane];
-  const uint32_t F0 = e0 >> 16, F1 = e1 >> 16, F2 = e2 >> 16, F3 = e3 >> 16;
-  const uint32_t R0 = chan(r0, e0, v0, m0, F0), G0 = chan(g0, e0, v0, m0, F0), Q0 = chan(b0, e0, v0, m0, F0);
-  const uint32_t R1 = chan(r1, e1, v1, m1, F1), G1 = chan(g1, e1, v1, m1, F1), Q1 = chan(b1, e1, v1, m1, F1);
-  const uint32_t R2 = chan(r2, e2, v2, m2, F2), G2 = chan(g2, e2, v2, m2, F2), Q2 = chan(b2, e2, v2, m2, F2);
-  const uint32_t R3 = chan(r3, e3, v3, m3, F3), G3 = chan(g3, e3, v3, m3, F3), Q3 = chan(b3, e3, v3, m3, F3);
+  const uint2 t0 = tab[v0], t1 = tab[v1], t2 = tab[v2], t3 = tab[v3];
+  const uint32_t F0 = t0.x >> 16, F1 = t1.x >> 16, F2 = t2.x >> 16, F3 = t3.x >> 16;
+  const uint32_t R0 = chan(r0, t0.x, v0, t0.y, F0), G0 = chan(g0, t0.x, v0, t0.y, F0), Q0 = chan(b0, t0.x, v0, t0.y, F0);
+  const uint32_t R1 = chan(r1, t1.x, v1, t1.y, F1), G1 = chan(g1, t1.x, v1, t1.y, F1), Q1 = chan(b1, t1.x, v1, t1.y, F1);
+  const uint32_t R2 = chan(r2, t2.x, v2, t2.y, F2), G2 = chan(g2, t2.x, v2, t2.y, F2), Q2 = chan(b2, t2.x, v2, t2.y, F2);
+  const uint32_t R3 = chan(r3, t3.x, v3, t3.y, F3), G3 = chan(g3, t3.x, v3, t3.y, F3), Q3 = chan(b3, t3.x, v3, t3.y, F3);
   o0 = __byte_perm(__byte_perm(R0, G0, 0x3340u), __byte_perm(Q0, R1, 0x3340u), 0x5410u);
   o1 = __byte_perm(__byte_perm(G1, Q1, 0x3340u), __byte_perm(R2, G2, 0x3340u), 0x5410u);
   o2 = __byte_perm(__byte_perm(Q2, R3, 0x3340u), __byte_perm(G3, Q3, 0x3340u), 0x5410u);
+}
+
+// per-warp (e, M) table of image b's LUT (lut read through L2: it may have been written by
+// another CTA of the same launch); the caller __syncwarp()s around it
+__device__ __forceinline__ void build_tab(uint2* tab, const uint8_t* __restrict__ lut_b, int lane) {
+#pragma unroll
+  for (int v = lane; v < kLevels; v += 32) tab[v] = make_uint2(ab_of(v, __ldcg(lut_b + v)), c_magic.m[v]);
 }
 
 // ---- PTX wrappers: mbarrier + bulk async copies (sm_90+, used on sm_100a) ----
@@ -119,27 +134,29 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 }
 
 struct __align__(128) ApplySmem {
-  uint8_t stage[kWarps][kStages][kChunkBytes];  // 60 KB
-  uint32_t mt[kLevels * 32];                    // 32 KB lane-private magic
-  uint32_t ab[kWarps][kLevels];                 // 8 KB per-warp (A | Bv << 16)
+  uint8_t stage[kWarps][kStages][kChunkBytes];  // 96 KB
+  uint2 tab[kWarps][kLevels];                   // 16 KB: per-warp (e, M)
   uint64_t bar[kWarps][kStages];
 };
 
-// One staged chunk (<= 512 px at p, `bytes` valid) transformed in place by the 32 lanes:
-// lane l owns pixels [16 l, 16 l + 16) -- three conflict-free 16-B LDS/STS at a 48-B stride.
-__device__ __forceinline__ void apply_chunk_smem(uint8_t* p, uint32_t bytes, const uint32_t* __restrict__ ab,
-                                                 const uint32_t* __restrict__ mt, int lane) {
-  if ((uint32_t)lane * 48u < bytes) {
-    uint4* q = reinterpret_cast<uint4*>(p + lane * 48);
-    const uint4 a = q[0], c = q[1], d = q[2];
-    uint4 x, y, z;
-    apply4(a.x, a.y, a.z, ab, mt, lane, x.x, x.y, x.z);
-    apply4(a.w, c.x, c.y, ab, mt, lane, x.w, y.x, y.y);
-    apply4(c.z, c.w, d.x, ab, mt, lane, y.z, y.w, z.x);
-    apply4(d.y, d.z, d.w, ab, mt, lane, z.y, z.z, z.w);
-    q[0] = x;
-    q[1] = y;
-    q[2] = z;
+// One staged chunk (<= 1024 px at p, `bytes` valid, a multiple of 48) transformed in place:
+// sub-block h in [0, 2), lane l owns pixels [512 h + 16 l, 512 h + 16 l + 16).
+__device__ __forceinline__ void apply_chunk_smem(uint8_t* p, uint32_t bytes, const uint2* __restrict__ tab, int lane) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t o = (uint32_t)h * kSubBytes + (uint32_t)lane * 48u;
+    if (o < bytes) {
+      uint4* q = reinterpret_cast<uint4*>(p + o);
+      const uint4 a = q[0], c = q[1], d = q[2];
+      uint4 x, y, z;
+      apply4(a.x, a.y, a.z, tab, x.x, x.y, x.z);
+      apply4(a.w, c.x, c.y, tab, x.w, y.x, y.y);
+      apply4(c.z, c.w, d.x, tab, y.z, y.w, z.x);
+      apply4(d.y, d.z, d.w, tab, z.y, z.z, z.w);
+      q[0] = x;
+      q[1] = y;
+      q[2] = z;
+    }
   }
 }
 

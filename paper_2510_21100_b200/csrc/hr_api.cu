@@ -460,7 +460,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     return cuda_err(c, e, "hr_enhance");
   }
   const int K = (int)std::min<int64_t>(c->chunks, B);
-  if (K <= 1 || ev) {  // serial on the caller's stream (also the stage-timed path)
+  if (K <= 1) {  // serial on the caller's stream (stage-timed: hist | solve + LUT | apply)
     if (e == cudaSuccess) e = mark(0);
     if (e == cudaSuccess) e = hist_chunk(0, B, st);
     if (e == cudaSuccess) e = mark(1);
@@ -481,6 +481,10 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     if (e == cudaSuccess) c->pev.push_back(x);
   }
   cudaEvent_t* E = c->pev.data();  // [0] fork, [1..3] joins, [4..4+K) hist done, [4+K..4+2K) solve done
+  // stage-timed: the whole pipeline is one stage (stage_ms = [0, 0, total])
+  if (e == cudaSuccess) e = mark(0);
+  if (e == cudaSuccess) e = mark(1);
+  if (e == cudaSuccess) e = mark(2);
   if (e == cudaSuccess) e = cudaEventRecord(E[0], st);
   for (cudaStream_t q : {c->sH, c->sS, c->sA})
     if (e == cudaSuccess) e = cudaStreamWaitEvent(q, E[0], 0);
@@ -500,6 +504,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, E[j], 0);
     ++j;
   }
+  if (e == cudaSuccess) e = mark(3);
   return cuda_err(c, e, "hr_enhance");
 }
 

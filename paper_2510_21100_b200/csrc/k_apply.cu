@@ -31,7 +31,6 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   extern __shared__ __align__(128) unsigned char smraw[];
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int i = tid; i < kLevels * 32; i += kApplyThreads) s.mt[i] = magic_of(i >> 5);
   if (lane == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&s.bar[w][k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -44,7 +43,7 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   // this warp's chunks: g0 + w, g0 + w + kWarps, ...
   const int mine = (g1 - g0 > (uint32_t)w) ? (int)((g1 - g0 - w + kWarps - 1) / kWarps) : 0;
   const uint64_t pol = policy_evict_first();
-  uint32_t* ab = s.ab[w];
+  uint2* tab = s.tab[w];
   int64_t cur_img = -1;
 
   // chunk cursor: image b, chunk c within the image; advances by kWarps chunks
@@ -90,7 +89,7 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
     where(cp, off, bytes);
     if ((int64_t)cp.b != cur_img) {  // per-warp LUT table for this image
       __syncwarp();
-      for (int v = lane; v < kLevels; v += 32) ab[v] = ab_of(v, lut[(uint64_t)cp.b * kLevels + v]);
+      build_tab(tab, lut + (uint64_t)cp.b * kLevels, lane);
       __syncwarp();
       cur_img = cp.b;
     }
@@ -103,7 +102,7 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
     }
     mbar_wait(&s.bar[w][st], ph);
     uint8_t* p = s.stage[w][st];
-    apply_chunk_smem(p, bytes, ab, s.mt, lane);
+    apply_chunk_smem(p, bytes, tab, lane);
     fence_async_smem();
     __syncwarp();
     if (lane == 0) {

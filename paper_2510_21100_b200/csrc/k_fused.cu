@@ -144,7 +144,6 @@ __global__ void __launch_bounds__(kFT, 2) k_fused(const FusedArgs a) {
 
   // ---------------- phase 2: per-warp TMA pipelines over dynamically ticketed chunk groups
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
-  for (int i = tid; i < kLevels * 32; i += kFT) s.mt[i] = magic_of(i >> 5);
   if (lane == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&s.bar[w][k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -155,7 +154,7 @@ __global__ void __launch_bounds__(kFT, 2) k_fused(const FusedArgs a) {
   const uint32_t total = (uint32_t)(a.B * (int64_t)cpi);  // < 2^31 (host-checked)
   const uint32_t ngroups = (total + GS - 1) / GS;
   const uint64_t pol = policy_evict_first();
-  uint32_t* ab = s.ab[w];
+  uint2* tab = s.tab[w];
   // loader state (lane 0): next chunk, end of its group, prefetched next group ticket
   uint32_t ldc = 0, lde = 0, nxt = 0;
   if (lane == 0) nxt = atomicAdd(a.ctl + 1, 1u);
@@ -223,12 +222,12 @@ __global__ void __launch_bounds__(kFT, 2) k_fused(const FusedArgs a) {
 #endif
       }
       __syncwarp();
-      for (int v = lane; v < kLevels; v += 32) ab[v] = ab_of(v, __ldcg(a.sa.lut + (uint64_t)bimg * kLevels + v));
+      build_tab(tab, a.sa.lut + (uint64_t)bimg * kLevels, lane);
       __syncwarp();
       cur_img = bimg;
     }
     uint8_t* p = s.stage[w][st];
-    apply_chunk_smem(p, bytes, ab, s.mt, lane);
+    apply_chunk_smem(p, bytes, tab, lane);
     fence_async_smem();
     __syncwarp();
     if (lane == 0) {

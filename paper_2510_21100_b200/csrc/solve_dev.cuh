@@ -375,6 +375,16 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   __syncthreads();
 }
 
+// sum of h[lo..hi] (hi - lo < kPiece): all loads predicated and in flight at once, fixed tree
+__device__ __forceinline__ double piece_sum(const double* __restrict__ h, int lo, int hi) {
+  static_assert(kPiece == 8, "tree below is for 8 cells");
+  const int n = hi - lo;
+  double x[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) x[m] = (m <= n) ? h[lo + m] : 0.0;
+  return ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
+}
+
 // sum over bin k of its pieces (contiguous, bin order: runs in row order)
 __device__ __forceinline__ double bin_sum(const Sm& s, const RunArena& A, int k) {
   double e0 = 0.0, e1 = 0.0;
@@ -442,14 +452,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       for (int p = tid; p < A.P; p += T) {  // piece sums hR_a * sum(hL over the piece)
         const uint32_t d = A.pDesc[p];
         const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;
-        double s0 = 0.0, s1 = 0.0;
-        int c = lo;
-        for (; c + 1 <= hi; c += 2) {
-          s0 += s.hL1[c];
-          s1 += s.hL1[c + 1];
-        }
-        if (c <= hi) s0 += s.hL1[c];
-        A.pVal[p] = s.hR1[pa] * (s0 + s1) * cRL;
+        A.pVal[p] = s.hR1[pa] * piece_sum(s.hL1, lo, hi) * cRL;
       }
       slot_put3(s, R_DR, dr, R_DL, dl, R_SL2, q);
     }
@@ -654,14 +657,7 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   for (int p = tid; p < A.P; p += T) {  // piece values hR_a * sum(hL over the piece)
     const uint32_t d = A.pDesc[p];
     const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;
-    double s0 = 0.0, s1 = 0.0;
-    int c = lo;
-    for (; c + 1 <= hi; c += 2) {
-      s0 += s.hL[c];
-      s1 += s.hL[c + 1];
-    }
-    if (c <= hi) s0 += s.hL[c];
-    A.pVal[p] = s.hR[pa] * (s0 + s1);
+    A.pVal[p] = s.hR[pa] * piece_sum(s.hL, lo, hi);
   }
   __syncthreads();
   double* Tt = s.rho;  // dense target

@@ -82,31 +82,38 @@ def summarise_launches(tag, spec):
     rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
-    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
-    times = defaultdict(list)
+    ki, mi, ui, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
+    us_scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    times, dram = defaultdict(list), defaultdict(float)
     for r in rows[hdr + 1:]:
-        if len(r) > vi:
-            k = r[ki]
-            for short in ("k_hist", "k_solve", "k_apply", "k_remap", "k_match"):
-                if short in k:
-                    k = short
-            times[k].append(num(r[vi]) / 1e3)
+        if len(r) <= vi:
+            continue
+        k = r[ki]
+        for short in ("k_fused", "k_hist", "k_solve_warp", "k_solve", "k_apply", "k_remap", "k_match", "k_idx1_table"):
+            if short in k:
+                k = short
+                break
+        if r[mi] == "gpu__time_duration.sum":
+            times[k].append(num(r[vi]) * us_scale.get(r[ui], 1e-3))
+        elif r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            dram[k] += to_bytes(r[vi], r[ui])
     tot = sum(sum(v) for v in times.values())
     name = f"{tag}_launches_{cfg}.txt"
     with open(os.path.join(PROF, name), "w") as f:
-        f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none launch list ({cfg}); "
-                "cold-cache, serialised: compare shares, not absolutes\n")
-        f.write(f"{'kernel':12s} {'launches':>8s} {'mean_us':>10s} {'min_us':>10s} {'share':>7s}\n")
+        f.write(f"# ncu --metrics gpu__time_duration.sum,dram__bytes_{{read,write}}.sum --clock-control none launch "
+                f"list ({cfg}); cold-cache, serialised: compare shares, not absolutes\n")
+        f.write(f"{'kernel':14s} {'launches':>8s} {'mean_us':>10s} {'min_us':>10s} {'share':>7s} {'dram_MB/launch':>15s}\n")
         for k, v in sorted(times.items(), key=lambda kv: -sum(kv[1])):
-            f.write(f"{k:12s} {len(v):8d} {sum(v)/len(v):10.2f} {min(v):10.2f} {sum(v)/tot:7.3f}\n")
+            f.write(f"{k:14s} {len(v):8d} {sum(v)/len(v):10.2f} {min(v):10.2f} {sum(v)/tot:7.3f} "
+                    f"{dram[k] / len(v) / 1e6:15.1f}\n")
     print("wrote", name)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", required=True)
-    ap.add_argument("--rep", nargs="*", default=[])
-    ap.add_argument("--launches", nargs="*", default=[])
+    ap.add_argument("--rep", action="extend", nargs="+", default=[])
+    ap.add_argument("--launches", action="extend", nargs="+", default=[])
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     tj = os.path.join(PROF, "ncu_traffic.json")
