@@ -131,8 +131,9 @@ hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_de
                    int32_t H, int32_t W, uint8_t* rgb_out_dev, void* stream);
 
 /* Steps (1)-(4) for the whole batch ("matching its histogram with the one provided by
-   HistRetinex") on `stream`.  Execution policy (hr_set_policy): for B >= fused_min_b (default
-   0 = off) with 16-byte aligned buffers and H*W % 16 == 0, ONE persistent kernel runs the
+   HistRetinex") on `stream`.  Execution policy (hr_set_policy): for fused_min_b <= B <=
+   fused_max_b (defaults 2 and #SMs/2) with 16-byte aligned buffers and H*W % 16 == 0, ONE
+   persistent kernel runs the
    histograms, each image's solve + LUT as soon as its histograms are complete, and the
    apply (solves overlap the streaming passes); otherwise the histogram, solve + LUT and
    apply kernels run in order (or as a chunk pipeline when chunks > 1).  Every policy gives
@@ -141,6 +142,20 @@ hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_de
    rgb_out must not alias rgb_in.  Workspace: hr_workspace_bytes(B,H,W), device. */
 hr_status hr_enhance(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H, int32_t W,
                      const hr_params* params, uint8_t* rgb_out_dev, void* ws_dev, void* stream);
+
+/* Steps (1)-(4) from HOST memory to HOST memory, pipelined over image chunks: chunk k's
+   host->device copy overlaps chunk k-1's enhancement (hr_enhance on `stream`) and chunk
+   k-2's device->host copy (PCIe is full duplex; the copies run on two library streams).
+   rgb_in_host, rgb_out_host: [B][H][W][3] host buffers, page-locked (cudaHostAlloc /
+   cudaHostRegister) for the copies to be asynchronous -- pageable memory still works but the
+   copies then serialise.  in_dev, out_dev: caller-owned device staging buffers of B*H*W*3
+   bytes each (reused across calls); ws_dev: hr_workspace_bytes(B, H, W).  chunks: number of
+   image chunks, 1..B (0 = min(B, 8)).  Enqueued on `stream`: rgb_out_host is complete when
+   `stream` reaches this point (e.g. after cudaStreamSynchronize).  The outputs are
+   bit-identical to hr_enhance on the same images.  rgb_out_host must not alias rgb_in_host. */
+hr_status hr_enhance_host(hr_ctx* ctx, const uint8_t* rgb_in_host, int64_t B, int32_t H, int32_t W,
+                          const hr_params* params, uint8_t* rgb_out_host, uint8_t* in_dev, uint8_t* out_dev,
+                          void* ws_dev, int32_t chunks, void* stream);
 
 hr_status hr_enhance_debug(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H,
                            int32_t W, const hr_params* params, uint8_t* rgb_out_dev, void* ws_dev,
@@ -160,10 +175,11 @@ hr_status hr_profile_enable(hr_ctx* ctx, int32_t on);
 hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
 
 /* Execution policy of hr_enhance (performance only: results never depend on it).  Keys:
-     "fused_min_b"  persistent fused kernel for B >= value (0: never)        default 0
+     "fused_min_b"  persistent fused kernel for B >= value (0: never)        default 2
+     "fused_max_b"  ... and B <= value (0: auto = #SMs / 2)                  default 0
      "fused_cpsm"   fused-kernel CTAs per SM (1..2)                           default 2
-     "fused_bands"  histogram band work items per CTA (1..2^20)            default 4
-     "fused_gs"     512-pixel chunks per apply work ticket (1..2^30)         default 4
+     "fused_bands"  histogram band work items per CTA (1..2^20)            default 2
+     "fused_gs"     1024-pixel chunks per apply work ticket (1..2^30)        default 8
      "chunks"       unfused path: image chunks of the stream pipeline (>= 1)  default 1
      "hist_cpsm", "apply_cpsm"  unfused kernels' CTAs per SM (1..2)         default 2
      "warp_solver"  unfused path: warp-per-image solver for small supports   default 0

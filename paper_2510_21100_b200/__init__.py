@@ -23,7 +23,7 @@ from ._lib import HrError
 
 __all__ = ["Params", "HrError", "hr_histogram", "hr_solve", "hr_match", "hr_apply", "hr_enhance",
            "hr_enhance_debug", "workspace_bytes", "version", "profile_enable", "profile_collect",
-           "set_policy", "kernel_launches"]
+           "set_policy", "kernel_launches", "hr_enhance_host"]
 
 
 @dataclass
@@ -206,6 +206,32 @@ def set_policy(key: str, value: int, device=None) -> None:
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     ctx = _context(dev)
     _check(_lib.load().hr_set_policy(ctx, key.encode(), int(value)), ctx)
+
+
+def hr_enhance_host(rgb_host: torch.Tensor, params: Params | None = None, out_host: torch.Tensor | None = None,
+                    device=None, chunks: int = 0, in_dev: torch.Tensor | None = None,
+                    out_dev: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                    sync: bool = True) -> torch.Tensor:
+    """hr_enhance_host: host [B, H, W, 3] uint8 in -> host out, copies pipelined with the
+    enhancement over image chunks.  Pinned (page-locked) host tensors make the copies
+    asynchronous.  Staging device buffers and the workspace are allocated when not given."""
+    if rgb_host.device.type != "cpu" or rgb_host.dtype != torch.uint8 or rgb_host.dim() != 4 or rgb_host.shape[-1] != 3:
+        raise ValueError("rgb_host must be a CPU uint8 tensor [B, H, W, 3]")
+    x = rgb_host.contiguous()
+    B, H, W, _ = x.shape
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    if out_host is None:
+        out_host = torch.empty_like(x, pin_memory=x.is_pinned())
+    in_dev = torch.empty(x.shape, dtype=torch.uint8, device=dev) if in_dev is None else in_dev
+    out_dev = torch.empty(x.shape, dtype=torch.uint8, device=dev) if out_dev is None else out_dev
+    ws = _workspace(B, H, W, dev) if workspace is None else workspace
+    pc = (params or Params()).c()
+    ctx = _context(dev)
+    _check(_lib.load().hr_enhance_host(ctx, _ptr(x), B, H, W, ctypes.byref(pc), _ptr(out_host), _ptr(in_dev),
+                                       _ptr(out_dev), _ptr(ws), int(chunks), _stream(dev)), ctx)
+    if sync:
+        torch.cuda.current_stream(dev).synchronize()
+    return out_host
 
 
 def kernel_launches(device=None) -> int:

@@ -18,7 +18,7 @@ EXPORTS = (
     "hr_default_params", "hr_create", "hr_destroy", "hr_status_string", "hr_last_error",
     "hr_version", "hr_workspace_bytes", "hr_histogram", "hr_solve", "hr_match", "hr_apply",
     "hr_enhance", "hr_enhance_debug", "hr_profile_enable", "hr_profile_collect", "hr_set_policy",
-    "hr_kernel_launches",
+    "hr_kernel_launches", "hr_enhance_host",
 )
 
 
@@ -74,6 +74,7 @@ def load() -> ctypes.CDLL:
         "hr_apply": ([vp, vp, vp, i64, i32, i32, vp, vp], i32),
         "hr_enhance": ([vp, vp, i64, i32, i32, P, vp, vp, vp], i32),
         "hr_enhance_debug": ([vp, vp, i64, i32, i32, P, vp, vp, vp, vp, vp, vp], i32),
+        "hr_enhance_host": ([vp, vp, i64, i32, i32, P, vp, vp, vp, vp, i32, vp], i32),
         "hr_profile_enable": ([vp, i32], i32),
         "hr_profile_collect": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)], i32),
         "hr_set_policy": ([vp, ctypes.c_char_p, i64], i32),

@@ -48,7 +48,8 @@ __host__ __device__ constexpr MagicTable make_magic() {
   for (int v = 0; v < kLevels; ++v) t.m[v] = magic_of(v);
   return t;
 }
-__constant__ MagicTable c_magic = make_magic();  // M[v], generated at compile time
+// M[v], generated at compile time; read through the read-only path (lanes read different v)
+__device__ const MagicTable g_magic = make_magic();
 
 // one pixel channel: floor((2 c V' + V) / 2V) = umulhi(c*e + V, M) + F
 __device__ __forceinline__ uint32_t chan(uint32_t c, uint32_t e, uint32_t v, uint32_t M, uint32_t F) {
@@ -79,7 +80,16 @@ __device__ __forceinline__ void apply4(uint32_t w0, uint32_t w1, uint32_t w2, co
 // another CTA of the same launch); the caller __syncwarp()s around it
 __device__ __forceinline__ void build_tab(uint2* tab, const uint8_t* __restrict__ lut_b, int lane) {
 #pragma unroll
-  for (int v = lane; v < kLevels; v += 32) tab[v] = make_uint2(ab_of(v, __ldcg(lut_b + v)), c_magic.m[v]);
+  for (int v = lane; v < kLevels; v += 32) tab[v] = make_uint2(ab_of(v, __ldcg(lut_b + v)), __ldg(&g_magic.m[v]));
+}
+// the same from LUT bytes [8 lane, 8 lane + 8) already in registers (lo: bytes 0-3, hi: 4-7)
+__device__ __forceinline__ void build_tab_regs(uint2* tab, uint2 lut8, int lane) {
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int v = 8 * lane + m;
+    const uint32_t L = (m < 4 ? lut8.x >> (8 * m) : lut8.y >> (8 * (m - 4))) & 0xFFu;
+    tab[v] = make_uint2(ab_of(v, L), __ldg(&g_magic.m[v]));
+  }
 }
 
 // ---- PTX wrappers: mbarrier + bulk async copies (sm_90+, used on sm_100a) ----

@@ -27,14 +27,17 @@ struct hr_ctx {
   int hist_cpsm = 2;      // k_hist CTAs per SM
   int apply_cpsm = 2;     // k_apply CTAs per SM
   int warp_solver = 0;    // 1: k_solve_warp for nR <= 32, k_solve for the rest; 0: k_solve only
-  int fused_min_b = 0;    // hr_enhance: persistent fused kernel for B >= this (0: never)
+  int fused_min_b = 2;    // hr_enhance: persistent fused kernel for B >= this (0: never) ...
+  int fused_max_b = 0;    // ... and B <= this (0: auto = SMs / 2: the solves' CTA slots stay cheap)
   int fused_cpsm = 2;     // k_fused CTAs per SM
-  int fused_bands = 4;    // histogram band items per CTA (sets bands per image)
-  int fused_gs = 4;       // 512-px chunks per apply ticket
+  int fused_bands = 2;    // histogram band items per CTA (sets bands per image)
+  int fused_gs = 8;       // 1024-px chunks per apply ticket
   int solve_cpsm = 0;     // k_solve CTAs per SM: 1, 2, or 0 = auto (1 when B <= SMs)
   int64_t launches = 0;   // kernels launched through this context (hr_kernel_launches)
   cudaStream_t sH = nullptr, sS = nullptr, sA = nullptr;
   std::vector<cudaEvent_t> pev;  // pipeline events
+  cudaStream_t sIn = nullptr, sOut = nullptr;  // hr_enhance_host copy streams
+  std::vector<cudaEvent_t> hev;                // hr_enhance_host events
   // stage timing (hr_profile_*)
   bool prof = false;
   int prof_used = 0;
@@ -186,10 +189,11 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_HIST_CPSM")) c->hist_cpsm = atoi(v) > 0 ? atoi(v) : 2;
   if (const char* v = getenv("HR_APPLY_CPSM")) c->apply_cpsm = atoi(v) > 0 ? atoi(v) : 2;
   if (const char* v = getenv("HR_WARP_SOLVER")) c->warp_solver = atoi(v) != 0;
-  if (const char* v = getenv("HR_FUSED_MIN_B")) c->fused_min_b = atoi(v) >= 0 ? atoi(v) : 0;
+  if (const char* v = getenv("HR_FUSED_MIN_B")) c->fused_min_b = atoi(v) >= 0 ? atoi(v) : 2;
+  if (const char* v = getenv("HR_FUSED_MAX_B")) c->fused_max_b = atoi(v) >= 0 ? atoi(v) : 0;
   if (const char* v = getenv("HR_FUSED_CPSM")) c->fused_cpsm = atoi(v) > 0 ? atoi(v) : 2;
-  if (const char* v = getenv("HR_FUSED_BANDS")) c->fused_bands = atoi(v) > 0 ? atoi(v) : 4;
-  if (const char* v = getenv("HR_FUSED_GS")) c->fused_gs = atoi(v) > 0 ? atoi(v) : 4;
+  if (const char* v = getenv("HR_FUSED_BANDS")) c->fused_bands = atoi(v) > 0 ? atoi(v) : 2;
+  if (const char* v = getenv("HR_FUSED_GS")) c->fused_gs = atoi(v) > 0 ? atoi(v) : 8;
   if (const char* v = getenv("HR_SOLVE_CPSM")) c->solve_cpsm = atoi(v) >= 0 && atoi(v) <= 2 ? atoi(v) : 0;
   *out = c;
   return HR_OK;
@@ -202,6 +206,9 @@ hr_status hr_destroy(hr_ctx* c) {
     if (c->sH) cudaStreamDestroy(c->sH);
     if (c->sS) cudaStreamDestroy(c->sS);
     if (c->sA) cudaStreamDestroy(c->sA);
+    for (cudaEvent_t e : c->hev) cudaEventDestroy(e);
+    if (c->sIn) cudaStreamDestroy(c->sIn);
+    if (c->sOut) cudaStreamDestroy(c->sOut);
     for (int i = 0; i < hr_ctx::kTab; ++i)
       if (c->idx1_tab[i]) cudaFree(c->idx1_tab[i]);
   }
@@ -227,7 +234,8 @@ hr_status hr_set_policy(hr_ctx* c, const char* key, int64_t v) {
     int64_t lo, hi;
   };
   const Knob knobs[] = {
-      {"fused_min_b", &c->fused_min_b, 0, 1 << 30}, {"fused_cpsm", &c->fused_cpsm, 1, 2},
+      {"fused_min_b", &c->fused_min_b, 0, 1 << 30}, {"fused_max_b", &c->fused_max_b, 0, 1 << 30},
+      {"fused_cpsm", &c->fused_cpsm, 1, 2},
       {"fused_bands", &c->fused_bands, 1, 1 << 20}, {"fused_gs", &c->fused_gs, 1, 1 << 30},
       {"chunks", &c->chunks, 1, 1 << 16},           {"hist_cpsm", &c->hist_cpsm, 1, 2},
       {"apply_cpsm", &c->apply_cpsm, 1, 2},         {"warp_solver", &c->warp_solver, 0, 1},
@@ -410,22 +418,25 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     a.grad_norm = p->grad_norm;
     a.p = *p;
     a.iters = iters_dbg ? iters_dbg + b0 : nullptr;
-    a.target = target + b0 * kLevels;
     a.cells_ws = cells + (size_t)b0 * (hr::solve_cells_ws_bytes(1));
     cudaError_t r = cudaSuccess;
-    if (c->warp_solver) {
+    if (c->warp_solver) {  // the warp solver writes the target; k_match then builds every LUT
+      a.target = target + b0 * kLevels;
       r = counted(c, hr::launch_solve_warp(a, nb, deferred + b0, s));
       a.only_deferred = deferred + b0;
+      if (r == cudaSuccess) r = counted(c, hr::launch_solve(a, nb, solve_cpsm_for(c, nb), s));
+      if (r == cudaSuccess) r = counted(c, hr::launch_match(a.hist_s, a.target, nb, lut + b0 * kLevels, nullptr, s));
+      return r;
     }
-    if (r == cudaSuccess) r = counted(c, hr::launch_solve(a, nb, solve_cpsm_for(c, nb), s));
-    if (r == cudaSuccess) r = counted(c, hr::launch_match(a.hist_s, a.target, nb, lut + b0 * kLevels, nullptr, s));
-    return r;
+    a.lut = lut + b0 * kLevels;  // CDF + LUT tail fused into the solver CTA (no target round trip)
+    return counted(c, hr::launch_solve(a, nb, solve_cpsm_for(c, nb), s));
   };
   auto apply_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
     return counted(c, hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s));
   };
   // persistent fused kernel: hist -> per-image solve + LUT -> apply, solves overlapped
-  if (c->fused_min_b > 0 && B >= c->fused_min_b && hr::fused_supported(in, out, B, H, W)) {
+  const int64_t fmax = c->fused_max_b > 0 ? c->fused_max_b : std::max(1, c->num_sms / 2);
+  if (c->fused_min_b > 0 && B >= c->fused_min_b && B <= fmax && hr::fused_supported(in, out, B, H, W)) {
     uint32_t* ctl = reinterpret_cast<uint32_t*>((char*)ws + L.ctl);
     if (e == cudaSuccess && hs != reinterpret_cast<uint32_t*>((char*)ws + L.hist_s))
       e = cudaMemsetAsync(hs, 0, (size_t)B * kLevels * sizeof(uint32_t), st);
@@ -511,6 +522,54 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
 hr_status hr_enhance(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, const hr_params* p,
                      uint8_t* out, void* ws, void* stream) {
   return hr_enhance_debug(c, in, B, H, W, p, out, ws, nullptr, nullptr, nullptr, stream);
+}
+
+hr_status hr_enhance_host(hr_ctx* c, const uint8_t* in_h, int64_t B, int32_t H, int32_t W, const hr_params* p,
+                          uint8_t* out_h, uint8_t* in_d, uint8_t* out_d, void* ws, int32_t chunks, void* stream) {
+  if (!c) return HR_EINVAL;
+  hr_status s = check_shape(c, B, H, W);
+  if (s) return s;
+  if ((s = check_params(c, p))) return s;
+  if (!in_h || !out_h || !in_d || !out_d || !ws) return set_err(c, HR_EINVAL, "NULL pointer");
+  if (in_h == out_h || in_d == out_d) return set_err(c, HR_EINVAL, "output must not alias input");
+  if (chunks < 0) return set_err(c, HR_EINVAL, "chunks must be >= 0");
+  if ((s = activate(c))) return s;
+  const int K = (int)std::min<int64_t>(chunks > 0 ? chunks : 8, B);
+  const size_t img = (size_t)H * W * 3;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (!c->sIn) e = cudaStreamCreateWithFlags(&c->sIn, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !c->sOut) e = cudaStreamCreateWithFlags(&c->sOut, cudaStreamNonBlocking);
+  while (e == cudaSuccess && (int)c->hev.size() < 2 * K + 2) {
+    cudaEvent_t x;
+    e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    if (e == cudaSuccess) c->hev.push_back(x);
+  }
+  if (e != cudaSuccess) return cuda_err(c, e, "hr_enhance_host");
+  cudaEvent_t* E = c->hev.data();  // [0] fork, [1] join, [2, 2+K) copied in, [2+K, 2+2K) enhanced
+  e = cudaEventRecord(E[0], st);  // everything earlier on `stream` (incl. the previous call) first
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->sIn, E[0], 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->sOut, E[0], 0);
+  for (int k = 0; k < K && e == cudaSuccess; ++k) {  // all host->device copies, in order
+    const int64_t b0 = B * k / K, nb = B * (k + 1) / K - b0;
+    e = cudaMemcpyAsync(in_d + b0 * img, in_h + b0 * img, nb * img, cudaMemcpyHostToDevice, c->sIn);
+    if (e == cudaSuccess) e = cudaEventRecord(E[2 + k], c->sIn);
+  }
+  for (int k = 0; k < K && e == cudaSuccess; ++k) {  // enhance chunk k once it is in, then copy it out
+    const int64_t b0 = B * k / K, nb = B * (k + 1) / K - b0;
+    e = cudaStreamWaitEvent(st, E[2 + k], 0);
+    if (e != cudaSuccess) break;
+    const hr_status r = hr_enhance_debug(c, in_d + b0 * img, nb, H, W, p, out_d + b0 * img, ws, nullptr, nullptr,
+                                         nullptr, stream);
+    if (r != HR_OK) return r;
+    e = cudaEventRecord(E[2 + K + k], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->sOut, E[2 + K + k], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out_h + b0 * img, out_d + b0 * img, nb * img, cudaMemcpyDeviceToHost, c->sOut);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(E[1], c->sOut);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, E[1], 0);
+  return cuda_err(c, e, "hr_enhance_host");
 }
 
 }  // extern "C"

@@ -174,16 +174,39 @@ __global__ void __launch_bounds__(kFT, 2) k_fused(const FusedArgs a) {
     off = ((uint64_t)bimg * (uint64_t)HW + px0) * 3u;
     bytes = npx * 3u;
   };
-  auto issue = [&](uint32_t i) {  // lane 0: fill stage i % kStages
+  // LUT prefetch: when the loader reaches the first chunk of a new image (kAhead chunks before
+  // the compute does), the warp acquires ready[b] and every lane loads its 8 LUT bytes into
+  // registers, so the table rebuild at the image switch needs no memory access.  At most one
+  // image is pending; a second switch inside the window takes the synchronous path.
+  uint32_t ld_img = kEnd;  // image of the last issued chunk
+  uint32_t pend_img = kEnd;
+  uint2 pend = make_uint2(0u, 0u);
+  auto issue = [&](uint32_t i) {  // all lanes (warp-uniform); lane 0 fills stage i % kStages
     const int st = (int)(i % kStages);
-    const uint32_t c = next_chunk();
-    meta[w][st] = c;
+    uint32_t c = 0;
+    if (lane == 0) c = next_chunk();
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (lane == 0) meta[w][st] = c;
     if (c == kEnd) {
-      mbar_arrive(&s.bar[w][st]);
-    } else {
-      uint32_t bimg, bytes;
-      uint64_t off;
-      locate(c, bimg, off, bytes);
+      if (lane == 0) mbar_arrive(&s.bar[w][st]);
+      return;
+    }
+    uint32_t bimg, bytes;
+    uint64_t off;
+    locate(c, bimg, off, bytes);
+    if (bimg != ld_img) {
+      ld_img = bimg;
+      if (pend_img == kEnd) {
+        uint32_t rdy = 0;
+        if (lane == 0) rdy = ld_acquire(ready + bimg);
+        __syncwarp();  // orders lane 0's acquire before the other lanes' LUT loads
+        if (__shfl_sync(0xffffffffu, rdy, 0)) {
+          pend = __ldcg(reinterpret_cast<const uint2*>(a.sa.lut + (uint64_t)bimg * kLevels) + lane);
+          pend_img = bimg;
+        }
+      }
+    }
+    if (lane == 0) {
       mbar_expect_tx(&s.bar[w][st], bytes);
       bulk_load(s.stage[w][st], a.in + off, bytes, &s.bar[w][st], pol);
     }
@@ -192,37 +215,41 @@ __global__ void __launch_bounds__(kFT, 2) k_fused(const FusedArgs a) {
 #ifdef HR_FUSED_TRACE
   TRACE_T(ta0);
 #endif
-  if (lane == 0)
-    for (uint32_t i = 0; i < (uint32_t)kAhead; ++i) issue(i);
+  for (uint32_t i = 0; i < (uint32_t)kAhead; ++i) issue(i);
   int64_t cur_img = -1;
   int st = 0;
   uint32_t ph = 0;
   for (uint32_t i = 0;; ++i) {
-    if (lane == 0) {
-      if (i >= 2) bulk_wait_read<1>();  // the store of chunk i-2 has left stage (i+kAhead)%kStages
-      issue(i + kAhead);
-    }
+    if (lane == 0 && i >= 2) bulk_wait_read<1>();  // the store of chunk i-2 has left stage (i+kAhead)%kStages
+    __syncwarp();
+    issue(i + kAhead);
     mbar_wait(&s.bar[w][st], ph);
     const uint32_t c = meta[w][st];
     if (c == kEnd) break;  // warp-uniform
     uint32_t bimg, bytes;
     uint64_t off;
     locate(c, bimg, off, bytes);
-    if ((int64_t)bimg != cur_img) {  // acquire image bimg's LUT, rebuild the per-warp table
-      if (lane == 0) {
-#ifdef HR_FUSED_TRACE
-        if (ld_acquire(ready + bimg) == 0u) {
-          TRACE_T(tw0);
-          while (ld_acquire(ready + bimg) == 0u) __nanosleep(200);
-          TRACE_T(tw1);
-          TRACE(3u, bimg, w, tw0, tw1);
-        }
-#else
-        while (ld_acquire(ready + bimg) == 0u) __nanosleep(200);
-#endif
-      }
+    if ((int64_t)bimg != cur_img) {  // image switch: rebuild the per-warp (e, M) table
       __syncwarp();
-      build_tab(tab, a.sa.lut + (uint64_t)bimg * kLevels, lane);
+      if (bimg == pend_img) {
+        build_tab_regs(tab, pend, lane);
+        pend_img = kEnd;
+      } else {
+        if (lane == 0) {
+#ifdef HR_FUSED_TRACE
+          if (ld_acquire(ready + bimg) == 0u) {
+            TRACE_T(tw0);
+            while (ld_acquire(ready + bimg) == 0u) __nanosleep(200);
+            TRACE_T(tw1);
+            TRACE(3u, bimg, w, tw0, tw1);
+          }
+#else
+          while (ld_acquire(ready + bimg) == 0u) __nanosleep(200);
+#endif
+        }
+        __syncwarp();
+        build_tab(tab, a.sa.lut + (uint64_t)bimg * kLevels, lane);
+      }
       __syncwarp();
       cur_img = bimg;
     }
@@ -273,7 +300,7 @@ size_t fused_smem_bytes() { return kFusedSmem; }
 cudaError_t launch_fused(FusedArgs a, int grid, cudaStream_t st) {
   const int64_t HW = (int64_t)a.H * a.W;
   a.cpi = (uint32_t)((HW + kChunkPx - 1) / kChunkPx);
-  if (a.GS < 1) a.GS = 4;
+  if (a.GS < 1) a.GS = 8;
   if (a.KB < 1) a.KB = 1;
   if (a.KB > a.H) a.KB = a.H;
   if (grid < 1) grid = 1;

@@ -29,7 +29,7 @@ def batch(B, H, W, seed0=0):
 
 def run(x, params=None, **policy):
     m = hr()
-    defaults = dict(fused_min_b=2, fused_cpsm=2, fused_bands=4, fused_gs=4)
+    defaults = dict(fused_min_b=2, fused_max_b=1 << 20, fused_cpsm=2, fused_bands=2, fused_gs=8)
     defaults.update(policy)
     for k, v in defaults.items():
         m.set_policy(k, v)
@@ -38,7 +38,7 @@ def run(x, params=None, **policy):
         torch.cuda.synchronize()
         return out.cpu().numpy(), hs.cpu().numpy(), lut.cpu().numpy(), it.cpu().numpy()
     finally:
-        for k, v in dict(fused_min_b=0, fused_cpsm=2, fused_bands=4, fused_gs=4).items():
+        for k, v in dict(fused_min_b=2, fused_max_b=0, fused_cpsm=2, fused_bands=2, fused_gs=8).items():
             m.set_policy(k, v)
 
 
@@ -128,3 +128,23 @@ def test_set_policy_rejects_bad_keys():
         m.set_policy("fused_cpsm", 3)
     with pytest.raises(m.HrError):
         m.set_policy("fused_gs", 0)
+
+
+@pytest.mark.parametrize("chunks", [0, 1, 3, 5])
+def test_enhance_host_equals_device(chunks):
+    """hr_enhance_host (pinned host in/out, copies pipelined over image chunks) gives exactly
+    hr_enhance's output; pageable host memory works too."""
+    m = hr()
+    x = batch(5, 40, 64, seed0=31)
+    ref = m.hr_enhance(torch.from_numpy(x).cuda()).cpu().numpy()
+    xp = torch.from_numpy(x).pin_memory()
+    got = m.hr_enhance_host(xp, chunks=chunks).numpy()
+    assert np.array_equal(got, ref)
+    got2 = m.hr_enhance_host(torch.from_numpy(x), chunks=chunks).numpy()  # pageable
+    assert np.array_equal(got2, ref)
+
+
+def test_enhance_host_rejects_bad_args():
+    m = hr()
+    with pytest.raises(ValueError):
+        m.hr_enhance_host(torch.zeros((2, 4, 4, 3), dtype=torch.uint8, device="cuda"))
