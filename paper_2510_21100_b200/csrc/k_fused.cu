@@ -306,6 +306,7 @@ cudaError_t launch_fused(FusedArgs a, int grid, cudaStream_t st) {
   if (grid < 1) grid = 1;
   const uintptr_t p = reinterpret_cast<uintptr_t>(a.in);
   if (p % 16 == 0 && a.W % 16 == 0) return launch_fv<16, 16>(a, grid, st);
+  if (p % 8 == 0 && a.W % 8 == 0 && a.W >= 16) return launch_fv<16, 8>(a, grid, st);
   if (p % 8 == 0 && a.W % 8 == 0) return launch_fv<8, 8>(a, grid, st);
   return launch_fv<16, 1>(a, grid, st);
 }

@@ -9,6 +9,8 @@
 // Design (B200): persistent grid of 2 CTAs/SM x 512 threads.  Each CTA owns a contiguous
 // range of global rows (all images concatenated), split at image boundaries into segments;
 // one flush per (CTA, image) segment with global integer atomics -> exact, deterministic.
+#include <cstdlib>
+
 #include "hist_dev.cuh"
 
 namespace hr {
@@ -48,6 +50,14 @@ cudaError_t launch_v(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32
   return cudaGetLastError();
 }
 
+bool hist_w8_strip16() {  // measurement switch: HR_HIST_W8=8 keeps the 8-px strips
+  static const int v = [] {
+    const char* e = getenv("HR_HIST_W8");
+    return e ? atoi(e) : 16;
+  }();
+  return v != 8;
+}
+
 }  // namespace
 
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
@@ -57,6 +67,8 @@ cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uin
   if (grid > rows) grid = (int)rows;
   if (grid < 1) grid = 1;
   if (a % 16 == 0 && W % 16 == 0) return launch_v<16, 16>(rgb, B, H, W, hist_s, hist_graw, grid, st);
+  // 8-B aligned rows: 16-px strips of six 8-B loads (the W % 16 == 8 remainder is the scalar tail)
+  if (a % 8 == 0 && W % 8 == 0 && W >= 16 && hist_w8_strip16()) return launch_v<16, 8>(rgb, B, H, W, hist_s, hist_graw, grid, st);
   if (a % 8 == 0 && W % 8 == 0) return launch_v<8, 8>(rgb, B, H, W, hist_s, hist_graw, grid, st);
   return launch_v<16, 1>(rgb, B, H, W, hist_s, hist_graw, grid, st);
 }
