@@ -188,9 +188,14 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
    Returns HR_EINVAL for an unknown key or an out-of-range value (nothing changes). */
 hr_status hr_set_policy(hr_ctx* ctx, const char* key, int64_t value);
 
-/* Number of CUDA kernels this context has launched so far (all entry points; memsets are
-   not kernels of this library and are not counted).  -1 for a NULL ctx. */
+/* Number of CUDA kernels this context has launched so far (all entry points, including the
+   accumulator-zeroing kernel; driver memsets are not counted).  -1 for a NULL ctx. */
 int64_t hr_kernel_launches(const hr_ctx* ctx);
+
+/* Execution path of the last hr_enhance on this context: 0 separate kernels (histogram |
+   solve + LUT | apply), 1 the persistent fused kernel, 2 the chunk pipeline; -1 none yet or
+   a NULL ctx. */
+int32_t hr_last_path(const hr_ctx* ctx);
 
 #ifdef __cplusplus
 }

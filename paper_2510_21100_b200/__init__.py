@@ -23,7 +23,7 @@ from ._lib import HrError
 
 __all__ = ["Params", "HrError", "hr_histogram", "hr_solve", "hr_match", "hr_apply", "hr_enhance",
            "hr_enhance_debug", "workspace_bytes", "version", "profile_enable", "profile_collect",
-           "set_policy", "kernel_launches", "hr_enhance_host"]
+           "set_policy", "kernel_launches", "hr_enhance_host", "last_path"]
 
 
 @dataclass
@@ -232,6 +232,12 @@ def hr_enhance_host(rgb_host: torch.Tensor, params: Params | None = None, out_ho
     if sync:
         torch.cuda.current_stream(dev).synchronize()
     return out_host
+
+
+def last_path(device=None) -> int:
+    """hr_last_path: 0 separate kernels, 1 fused kernel, 2 chunk pipeline (last hr_enhance)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    return int(_lib.load().hr_last_path(_context(dev)))
 
 
 def kernel_launches(device=None) -> int:

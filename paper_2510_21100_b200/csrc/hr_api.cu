@@ -34,6 +34,7 @@ struct hr_ctx {
   int fused_gs = 8;       // 1024-px chunks per apply ticket
   int solve_cpsm = 0;     // k_solve CTAs per SM: 1, 2, or 0 = auto (1 when B <= SMs)
   int64_t launches = 0;   // kernels launched through this context (hr_kernel_launches)
+  int last_path = -1;     // hr_last_path: 0 separate kernels, 1 fused, 2 chunk pipeline
   cudaStream_t sH = nullptr, sS = nullptr, sA = nullptr;
   std::vector<cudaEvent_t> pev;  // pipeline events
   cudaStream_t sIn = nullptr, sOut = nullptr;  // hr_enhance_host copy streams
@@ -224,6 +225,7 @@ hr_status hr_profile_enable(hr_ctx* c, int32_t on) {
 }
 
 int64_t hr_kernel_launches(const hr_ctx* c) { return c ? c->launches : -1; }
+int32_t hr_last_path(const hr_ctx* c) { return c ? c->last_path : -1; }
 
 hr_status hr_set_policy(hr_ctx* c, const char* key, int64_t v) {
   if (!c) return HR_EINVAL;
@@ -404,8 +406,8 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   const size_t img = (size_t)H * W * 3;
   // one chunk of images [b0, b0 + nb): histograms | solve + LUT | apply, each on its stream
   auto hist_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
-    cudaError_t r = cudaMemsetAsync(hs + b0 * kLevels, 0, (size_t)nb * kLevels * sizeof(uint32_t), s);
-    if (r == cudaSuccess) r = cudaMemsetAsync(graw + b0 * kGradSlots, 0, (size_t)nb * kGradSlots * sizeof(uint32_t), s);
+    cudaError_t r = counted(c, hr::launch_zero(hs + b0 * kLevels, (size_t)nb * kLevels * sizeof(uint32_t), s));
+    if (r == cudaSuccess) r = counted(c, hr::launch_zero(graw + b0 * kGradSlots, (size_t)nb * kGradSlots * sizeof(uint32_t), s));
     if (r == cudaSuccess) r = counted(c, hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, hist_grid(c), s));
     return r;
   };
@@ -439,10 +441,10 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   if (c->fused_min_b > 0 && B >= c->fused_min_b && B <= fmax && hr::fused_supported(in, out, B, H, W)) {
     uint32_t* ctl = reinterpret_cast<uint32_t*>((char*)ws + L.ctl);
     if (e == cudaSuccess && hs != reinterpret_cast<uint32_t*>((char*)ws + L.hist_s))
-      e = cudaMemsetAsync(hs, 0, (size_t)B * kLevels * sizeof(uint32_t), st);
+      e = counted(c, hr::launch_zero(hs, (size_t)B * kLevels * sizeof(uint32_t), st));
     const size_t z0 = hs == reinterpret_cast<uint32_t*>((char*)ws + L.hist_s) ? L.hist_s : L.graw;
     if (e == cudaSuccess) e = mark(0);
-    if (e == cudaSuccess) e = cudaMemsetAsync((char*)ws + z0, 0, L.ctl + hr::fused_ctl_bytes(B) - z0, st);
+    if (e == cudaSuccess) e = counted(c, hr::launch_zero((char*)ws + z0, align_up(L.ctl + hr::fused_ctl_bytes(B)) - z0, st));
     if (e == cudaSuccess) e = mark(1);
     hr::FusedArgs f{};
     f.in = in;
@@ -466,11 +468,13 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     f.KB = (int32_t)std::max<int64_t>(1, std::min<int64_t>(kb, std::max(1, H / 16)));
     f.GS = (uint32_t)c->fused_gs;
     if (e == cudaSuccess) e = counted(c, hr::launch_fused(f, grid, st));
+    c->last_path = 1;
     if (e == cudaSuccess) e = mark(2);
     if (e == cudaSuccess) e = mark(3);
     return cuda_err(c, e, "hr_enhance");
   }
   const int K = (int)std::min<int64_t>(c->chunks, B);
+  c->last_path = K <= 1 ? 0 : 2;
   if (K <= 1) {  // serial on the caller's stream (stage-timed: hist | solve + LUT | apply)
     if (e == cudaSuccess) e = mark(0);
     if (e == cudaSuccess) e = hist_chunk(0, B, st);

@@ -4,10 +4,44 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "../../include/histretinex.h"
 
 namespace hr {
+
+// ---- programmatic dependent launch (PDL) ----
+// Kernels of a step are launched with programmatic stream serialization: a kernel's launch
+// (CTA rasterisation, shared-memory carve-out) overlaps its predecessor's tail.  Every such
+// kernel calls pdl_wait() before touching memory, which returns once the predecessor grid has
+// completed and its writes are visible (a no-op for a normal launch), then pdl_trigger() so
+// that its own successor may launch early.  HR_PDL=0 disables the attribute (A/B timing).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HR_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 constexpr int kLevels = 256;     // l (the only level count of this build)
 constexpr int kGradSlots = 512;  // raw gradient |dx|+|dy| in [0, 510]
@@ -61,6 +95,8 @@ cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
                          uint8_t* out, int grid_ctas, cudaStream_t st);
+// zero n bytes (n % 16 == 0, 16-B aligned) -- replaces cudaMemsetAsync inside the PDL chain
+cudaError_t launch_zero(void* p, size_t n, cudaStream_t st);
 
 // Persistent fused kernel (k_fused.cu): histograms -> per-image solve + LUT -> apply.
 constexpr int kCtlHeader = 32;  // control words before done[B]

@@ -31,6 +31,8 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   extern __shared__ __align__(128) unsigned char smraw[];
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  pdl_wait();
+  pdl_trigger();
   if (lane == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&s.bar[w][k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -166,7 +168,8 @@ cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32
     int64_t grid = grid_ctas;
     if (grid > (chunks + kWarps - 1) / kWarps) grid = (chunks + kWarps - 1) / kWarps;
     if (grid < 1) grid = 1;
-    k_apply_tma<<<(unsigned)grid, kApplyThreads, sizeof(ApplySmem), st>>>(in, lut, B, HW, out);
+    return launch_pdl(k_apply_tma, dim3((unsigned)grid), dim3(kApplyThreads), sizeof(ApplySmem), st, in, lut, B, HW,
+                      out);
   } else {
     int64_t grid = 4LL * grid_ctas;
     const int64_t P = B * HW;

@@ -88,6 +88,8 @@ __global__ void __launch_bounds__(kFT, 2) k_fused(const FusedArgs a) {
   const size_t imgBytes = (size_t)HW * 3;
   uint32_t* done = a.ctl + kCtlHeader;
   uint32_t* ready = done + a.B;
+  pdl_wait();
+  pdl_trigger();
 #ifdef HR_FUSED_TRACE
   if (tid == 0) {
     TRACE_T(tk);
@@ -283,8 +285,7 @@ cudaError_t launch_fv(const FusedArgs& a, int grid, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_fused<SW, VEC><<<grid, kFT, kFusedSmem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_fused<SW, VEC>, dim3(grid), dim3(kFT), kFusedSmem, st, a);
 }
 
 }  // namespace

@@ -9,6 +9,7 @@
 // Design (B200): persistent grid of 2 CTAs/SM x 512 threads.  Each CTA owns a contiguous
 // range of global rows (all images concatenated), split at image boundaries into segments;
 // one flush per (CTA, image) segment with global integer atomics -> exact, deterministic.
+#include <algorithm>
 #include <cstdlib>
 
 #include "hist_dev.cuh"
@@ -21,6 +22,8 @@ __global__ void __launch_bounds__(kHistThreads, 2)
 k_hist(const uint8_t* __restrict__ rgb, int64_t B, int H, int W, uint32_t* __restrict__ hist_s,
        uint32_t* __restrict__ hist_graw) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_wait();
+  pdl_trigger();
   const int64_t R = B * (int64_t)H;
   const int64_t r_begin = R * blockIdx.x / gridDim.x;
   const int64_t r_end = R * (blockIdx.x + 1) / gridDim.x;
@@ -46,8 +49,7 @@ cudaError_t launch_v(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_hist<SW, VEC><<<grid, kHistThreads, kHistDevSmem, st>>>(rgb, B, H, W, hs, hg);
-  return cudaGetLastError();
+  return launch_pdl(k_hist<SW, VEC>, dim3(grid), dim3(kHistThreads), kHistDevSmem, st, rgb, B, H, W, hs, hg);
 }
 
 bool hist_w8_strip16() {  // measurement switch: HR_HIST_W8=8 keeps the 8-px strips
@@ -58,7 +60,21 @@ bool hist_w8_strip16() {  // measurement switch: HR_HIST_W8=8 keeps the 8-px str
   return v != 8;
 }
 
+__global__ void __launch_bounds__(256) k_zero(uint4* __restrict__ p, size_t n16) {
+  pdl_wait();
+  pdl_trigger();
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 }  // namespace
+
+cudaError_t launch_zero(void* p, size_t n, cudaStream_t st) {
+  const size_t n16 = n / 16;
+  if (n16 == 0) return cudaSuccess;
+  const size_t grid = std::min<size_t>((n16 + 255) / 256, 1024);
+  return launch_pdl(k_zero, dim3((unsigned)grid), dim3(256), 0, st, reinterpret_cast<uint4*>(p), n16);
+}
 
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
                         uint32_t* hist_graw, int grid, cudaStream_t st) {

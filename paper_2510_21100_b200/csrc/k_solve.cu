@@ -13,6 +13,8 @@ namespace {
 __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int wscr[NW];
+  pdl_wait();
+  pdl_trigger();
   solve_image(args, blockIdx.x, smraw, wscr);
 }
 
@@ -65,8 +67,7 @@ cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t s
     attr = true;
   }
   const size_t smem = cpsm == 1 ? std::max(solve_smem_bytes(), kOnePerSm) : solve_smem_bytes();
-  k_solve<<<(unsigned)B, T, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_solve, dim3((unsigned)B), dim3(T), smem, st, a);
 }
 
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st) {

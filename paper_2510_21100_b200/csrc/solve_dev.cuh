@@ -77,7 +77,7 @@ constexpr int kProfBlock = 0;
 #endif
 
 // slots of the block-reduction scratch
-enum { R_SL2 = 0, R_SR1, R_SR2, R_SL1, R_DR, R_DL, kSlots };
+enum { R_SL2 = 0, R_SR1, R_SR2, R_SL1, R_DR, R_DL, R_QL1, kSlots };
 
 struct __align__(16) Sm {
   double hR[kLevels], hL[kLevels];    // renormalised state (index a over sR, c over sL)
@@ -425,6 +425,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
   const int form = P.update_form;
   const double invN = 1.0 / N, invN2 = invN * invN;
   double SR1 = N, SL1 = N;  // sums of the raw iterates (initially exactly N)
+  double QL1 = 0.0;          // sum of the raw hL iterate squared (from the L phase, t > 0)
   int t = 0;
 #ifdef HR_SOLVE_PROFILE
   long long pacc[6] = {0, 0, 0, 0, 0, 0}, pt0 = clock64(), pt1;
@@ -433,9 +434,12 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
 #define PHASE(i) do { } while (0)
 #endif
   for (;;) {
-    // ======== E1: renormalise (Eqs. 15, 14); run sums of hL and hL^2 (Eqs. 6, 8) ========
+    // ======== E1: renormalise (Eqs. 15, 14); piece sums (Eqs. 6, 8) ========
+    // sum hL^2 of the renormalised hL = cL^2 * QL1 (reduced in the L phase); the block
+    // reduction here is only needed for t = 0 and for the stop rule
+    const double cL = N * rcp_fast(SL1);
     {
-      const double cR = N * rcp_fast(SR1), cL = N * rcp_fast(SL1), cRL = cR * cL;
+      const double cR = N * rcp_fast(SR1), cRL = cR * cL;
       double dr = 0.0, dl = 0.0, q = 0.0;
       if (tid < nR) {
         const double n = cR * s.hR1[tid];
@@ -454,7 +458,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;
         A.pVal[p] = s.hR1[pa] * piece_sum(s.hL1, lo, hi) * cRL;
       }
-      slot_put3(s, R_DR, dr, R_DL, dl, R_SL2, q);
+      if (t == 0 || P.use_epsilon) slot_put3(s, R_DR, dr, R_DL, dl, R_SL2, q);
     }
     __syncthreads();
     PHASE(0);
@@ -471,7 +475,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         s.rho[k] = form == 0 ? (e > 0.0 ? s.hSd[k] * rcp_fast(e) : 0.0) : s.hSd[k] * e;
       }
     }
-    const double invDenR = rcp_fast(slot_sum(s, R_SL2) * invN2 + P.beta);
+    const double invDenR = rcp_fast((t == 0 ? slot_sum(s, R_SL2) : cL * cL * QL1) * invN2 + P.beta);
     __syncthreads();
     PHASE(1);
     // ======== R: Eq. 13, TPR threads per row walking every TPR-th cell, fixed-order reduce ========
@@ -534,13 +538,14 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         u = u > 0.0 ? u : 0.0;
         s.hL1[c] = u;
       }
-      slot_put3(s, R_SL1, u, -1, 0.0, -1, 0.0);
+      slot_put3(s, R_SL1, u, R_QL1, u * u, -1, 0.0);
     }
     __syncthreads();
     PHASE(3);
     ++t;
     SR1 = slot_sum(s, R_SR1);
     SL1 = slot_sum(s, R_SL1);
+    QL1 = slot_sum(s, R_QL1);
   }
 #ifdef HR_SOLVE_PROFILE
   if (blockIdx.x == kProfBlock && threadIdx.x == 0)
