@@ -293,7 +293,7 @@ def run_ours(args, world, rank, local):
             step()
         (h_ms, s_ms, a_ms), n2 = hr.profile_collect(local)
         hr.profile_enable(local, False)
-        hr.set_policy("fused_min_b", int(os.environ.get("HR_FUSED_MIN_B", "2")), local)
+        hr.set_policy("fused_min_b", int(os.environ.get("HR_FUSED_MIN_B", "0")), local)
         hr.set_policy("chunks", max(1, int(os.environ.get("HR_CHUNKS", "1"))), local)
         split = (h_ms / max(n2, 1), s_ms / max(n2, 1), a_ms / max(n2, 1))
     else:

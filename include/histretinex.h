@@ -131,9 +131,11 @@ hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_de
                    int32_t H, int32_t W, uint8_t* rgb_out_dev, void* stream);
 
 /* Steps (1)-(4) for the whole batch ("matching its histogram with the one provided by
-   HistRetinex") on `stream`.  Execution policy (hr_set_policy): for fused_min_b <= B <=
-   fused_max_b (defaults 2 and #SMs/2) with 16-byte aligned buffers and H*W % 16 == 0, ONE
-   persistent kernel runs the
+   HistRetinex") on `stream`.  Default: the histogram, solve + LUT and apply kernels in order,
+   chained by programmatic dependent launch, the apply acquiring each image's LUT-ready flag
+   (so it overlaps the solver's tail).  Policy (hr_set_policy): for fused_min_b <= B <=
+   fused_max_b (fused_min_b = 0 = off by default) with 16-byte aligned buffers and
+   H*W % 16 == 0, ONE persistent kernel runs the
    histograms, each image's solve + LUT as soon as its histograms are complete, and the
    apply (solves overlap the streaming passes); otherwise the histogram, solve + LUT and
    apply kernels run in order (or as a chunk pipeline when chunks > 1).  Every policy gives
@@ -175,7 +177,7 @@ hr_status hr_profile_enable(hr_ctx* ctx, int32_t on);
 hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
 
 /* Execution policy of hr_enhance (performance only: results never depend on it).  Keys:
-     "fused_min_b"  persistent fused kernel for B >= value (0: never)        default 2
+     "fused_min_b"  persistent fused kernel for B >= value (0: never)        default 0
      "fused_max_b"  ... and B <= value (0: auto = #SMs / 2)                  default 0
      "fused_cpsm"   fused-kernel CTAs per SM (1..2)                           default 2
      "fused_bands"  histogram band work items per CTA (1..2^20)            default 2

@@ -27,7 +27,7 @@ struct hr_ctx {
   int hist_cpsm = 2;      // k_hist CTAs per SM
   int apply_cpsm = 2;     // k_apply CTAs per SM
   int warp_solver = 0;    // 1: k_solve_warp for nR <= 32, k_solve for the rest; 0: k_solve only
-  int fused_min_b = 2;    // hr_enhance: persistent fused kernel for B >= this (0: never) ...
+  int fused_min_b = 0;    // hr_enhance: persistent fused kernel for B >= this (0: never) ...
   int fused_max_b = 0;    // ... and B <= this (0: auto = SMs / 2: the solves' CTA slots stay cheap)
   int fused_cpsm = 2;     // k_fused CTAs per SM
   int fused_bands = 2;    // histogram band items per CTA (sets bands per image)
@@ -190,7 +190,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_HIST_CPSM")) c->hist_cpsm = atoi(v) > 0 ? atoi(v) : 2;
   if (const char* v = getenv("HR_APPLY_CPSM")) c->apply_cpsm = atoi(v) > 0 ? atoi(v) : 2;
   if (const char* v = getenv("HR_WARP_SOLVER")) c->warp_solver = atoi(v) != 0;
-  if (const char* v = getenv("HR_FUSED_MIN_B")) c->fused_min_b = atoi(v) >= 0 ? atoi(v) : 2;
+  if (const char* v = getenv("HR_FUSED_MIN_B")) c->fused_min_b = atoi(v) >= 0 ? atoi(v) : 0;
   if (const char* v = getenv("HR_FUSED_MAX_B")) c->fused_max_b = atoi(v) >= 0 ? atoi(v) : 0;
   if (const char* v = getenv("HR_FUSED_CPSM")) c->fused_cpsm = atoi(v) > 0 ? atoi(v) : 2;
   if (const char* v = getenv("HR_FUSED_BANDS")) c->fused_bands = atoi(v) > 0 ? atoi(v) : 2;
@@ -411,8 +411,9 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     if (r == cudaSuccess) r = counted(c, hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, hist_grid(c), s));
     return r;
   };
-  auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
+  auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, uint32_t* ready = nullptr) -> cudaError_t {
     hr::SolveArgs a{};
+    a.ready = c->warp_solver ? nullptr : ready;
     a.idx1_tab = tab;
     a.hist_s = hs + b0 * kLevels;
     a.hist_g = nullptr;
@@ -433,8 +434,9 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     a.lut = lut + b0 * kLevels;  // CDF + LUT tail fused into the solver CTA (no target round trip)
     return counted(c, hr::launch_solve(a, nb, solve_cpsm_for(c, nb), s));
   };
-  auto apply_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
-    return counted(c, hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s));
+  auto apply_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, const uint32_t* ready = nullptr) -> cudaError_t {
+    return counted(c, hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s,
+                                       c->warp_solver ? nullptr : ready));
   };
   // persistent fused kernel: hist -> per-image solve + LUT -> apply, solves overlapped
   const int64_t fmax = c->fused_max_b > 0 ? c->fused_max_b : std::max(1, c->num_sms / 2);
@@ -476,12 +478,38 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   const int K = (int)std::min<int64_t>(c->chunks, B);
   c->last_path = K <= 1 ? 0 : 2;
   if (K <= 1) {  // serial on the caller's stream (stage-timed: hist | solve + LUT | apply)
+    // per-image LUT-ready flags (in the zeroed control block) let the apply grid, launched
+    // early under PDL, start on images whose LUT is done while the solver grid finishes
+    static const bool use_ready = [] {
+      const char* v = getenv("HR_READY");
+      return !(v && atoi(v) == 0);
+    }();
+    uint32_t* ready = use_ready ? reinterpret_cast<uint32_t*>((char*)ws + L.ctl) + hr::kCtlHeader + B : nullptr;
+    const bool own_hs = hs == reinterpret_cast<uint32_t*>((char*)ws + L.hist_s);
+    const size_t z0 = own_hs ? L.hist_s : L.graw;
+    // zeroing as separate launches per region: measured faster in the PDL chain than one launch
+    // over [hist_s | graw | ctl] (C5 0.165 vs 0.174 ms; HR_ZERO2=0 selects the single launch)
+    static const bool zero2 = [] {
+      const char* v = getenv("HR_ZERO2");
+      return !(v && atoi(v) == 0);
+    }();
     if (e == cudaSuccess) e = mark(0);
-    if (e == cudaSuccess) e = hist_chunk(0, B, st);
+    if (zero2) {
+      if (e == cudaSuccess) e = counted(c, hr::launch_zero(hs, (size_t)B * kLevels * sizeof(uint32_t), st));
+      if (e == cudaSuccess) e = counted(c, hr::launch_zero(graw, (size_t)B * kGradSlots * sizeof(uint32_t), st));
+      if (e == cudaSuccess && ready)  // the whole (256-B aligned) control block holding ready[]
+        e = counted(c, hr::launch_zero((char*)ws + L.ctl, align_up(hr::fused_ctl_bytes(B)), st));
+    } else {
+      if (e == cudaSuccess && !own_hs) e = counted(c, hr::launch_zero(hs, (size_t)B * kLevels * sizeof(uint32_t), st));
+      if (e == cudaSuccess)
+        e = counted(c, hr::launch_zero((char*)ws + z0, align_up(L.ctl + hr::fused_ctl_bytes(B)) - z0, st));
+    }
+    if (e == cudaSuccess)
+      e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st));
     if (e == cudaSuccess) e = mark(1);
-    if (e == cudaSuccess) e = solve_chunk(0, B, st);
+    if (e == cudaSuccess) e = solve_chunk(0, B, st, ready);
     if (e == cudaSuccess) e = mark(2);
-    if (e == cudaSuccess) e = apply_chunk(0, B, st);
+    if (e == cudaSuccess) e = apply_chunk(0, B, st, ready);
     if (e == cudaSuccess) e = mark(3);
     return cuda_err(c, e, "hr_enhance");
   }

@@ -27,6 +27,15 @@ inline bool pdl_enabled() {
   }();
   return on;
 }
+// gpu-scope acquire / release on a 32-bit flag (LUT-ready handshakes between CTAs and grids)
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -82,6 +91,7 @@ struct SolveArgs {
   unsigned char* cells_ws;  // [B][kArenaGlobal] run arenas of images whose runs exceed shared memory
   const uint8_t* idx1_tab;  // [256][256] index_1(i, j) for params.gamma (launch_idx1_table)
   const int32_t* only_deferred;  // k_solve: when set, images with only_deferred[b] == 0 are skipped
+  uint32_t* ready;               // [B] nullable (k_solve): released (= 1) once image b's LUT is written
 };
 // warp-per-image solver for nR <= 32; flags the other images in deferred[b] (then run k_solve)
 cudaError_t launch_solve_warp(const SolveArgs& a, int64_t B, int32_t* deferred, cudaStream_t st);
@@ -93,8 +103,10 @@ size_t solve_cells_ws_bytes(int64_t B);
 cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,
                          int32_t* status, cudaStream_t st);
 
+// ready (nullable): per-image LUT-ready flags released by k_solve; when given, the TMA apply
+// does not wait for the solver grid to finish but acquires ready[b] before image b's table
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
-                         uint8_t* out, int grid_ctas, cudaStream_t st);
+                         uint8_t* out, int grid_ctas, cudaStream_t st, const uint32_t* ready = nullptr);
 // zero n bytes (n % 16 == 0, 16-B aligned) -- replaces cudaMemsetAsync inside the PDL chain
 cudaError_t launch_zero(void* p, size_t n, cudaStream_t st);
 

@@ -27,11 +27,11 @@ namespace {
 
 __global__ void __launch_bounds__(kApplyThreads, 2)
 k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int64_t B, int64_t HW,
-            uint8_t* __restrict__ out) {
+            uint8_t* __restrict__ out, const uint32_t* __restrict__ ready) {
   extern __shared__ __align__(128) unsigned char smraw[];
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  pdl_wait();
+  if (!ready) pdl_wait();  // with per-image flags only the LUTs depend on the solver grid
   pdl_trigger();
   if (lane == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&s.bar[w][k], 1);
@@ -90,6 +90,9 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
     uint32_t bytes;
     where(cp, off, bytes);
     if ((int64_t)cp.b != cur_img) {  // per-warp LUT table for this image
+      __syncwarp();
+      if (ready && lane == 0)
+        while (ld_acquire(ready + cp.b) == 0u) __nanosleep(100);
       __syncwarp();
       build_tab(tab, lut + (uint64_t)cp.b * kLevels, lane);
       __syncwarp();
@@ -152,7 +155,7 @@ k_apply_scalar(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, 
 }  // namespace
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
-                         int grid_ctas, cudaStream_t st) {
+                         int grid_ctas, cudaStream_t st, const uint32_t* ready) {
   const int64_t HW = (int64_t)H * W;
   const bool tma = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                    (HW % 16 == 0) && B * ((HW + kChunkPx - 1) / kChunkPx) < (1LL << 31);
@@ -169,7 +172,7 @@ cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32
     if (grid > (chunks + kWarps - 1) / kWarps) grid = (chunks + kWarps - 1) / kWarps;
     if (grid < 1) grid = 1;
     return launch_pdl(k_apply_tma, dim3((unsigned)grid), dim3(kApplyThreads), sizeof(ApplySmem), st, in, lut, B, HW,
-                      out);
+                      out, ready);
   } else {
     int64_t grid = 4LL * grid_ctas;
     const int64_t P = B * HW;

@@ -16,6 +16,11 @@ __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
   pdl_wait();
   pdl_trigger();
   solve_image(args, blockIdx.x, smraw, wscr);
+  if (args.ready) {  // every exit of solve_image arrives here: LUT written -> release ready[b]
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(args.ready + blockIdx.x, 1u);
+  }
 }
 
 // index_1(i, j) of Eqs. 17-19 for every (i, j), once per gamma (R4, R5):

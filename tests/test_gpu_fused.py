@@ -38,7 +38,7 @@ def run(x, params=None, **policy):
         torch.cuda.synchronize()
         return out.cpu().numpy(), hs.cpu().numpy(), lut.cpu().numpy(), it.cpu().numpy()
     finally:
-        for k, v in dict(fused_min_b=2, fused_max_b=0, fused_cpsm=2, fused_bands=2, fused_gs=8).items():
+        for k, v in dict(fused_min_b=0, fused_max_b=0, fused_cpsm=2, fused_bands=2, fused_gs=8).items():
             m.set_policy(k, v)
 
 

@@ -71,4 +71,4 @@ def run(cfg, policy):
 
 
 for cfg in sys.argv[1:] or ["C3", "C5"]:
-    run(cfg, {"fused_min_b": 2, "fused_bands": 4, "fused_gs": 4, "fused_cpsm": 2})
+    run(cfg, {"fused_min_b": 2, "fused_max_b": 1 << 20, "fused_bands": 2, "fused_gs": 8, "fused_cpsm": 2})
