@@ -33,6 +33,8 @@ struct hr_ctx {
   int fused_bands = 2;    // histogram band items per CTA (sets bands per image)
   int fused_gs = 8;       // 1024-px chunks per apply ticket
   int solve_cpsm = 0;     // k_solve CTAs per SM: 1, 2, or 0 = auto (1 when B <= SMs)
+  int hist_overlap = 0;   // separate kernels: solves start per image beside a 2x256-thread histogram pass
+                          // (off: the 16-warp histogram pass costs more than the overlap saves)
   int64_t launches = 0;   // kernels launched through this context (hr_kernel_launches)
   int last_path = -1;     // hr_last_path: 0 separate kernels, 1 fused, 2 chunk pipeline
   cudaStream_t sH = nullptr, sS = nullptr, sA = nullptr;
@@ -51,6 +53,8 @@ using hr::kGradSlots;
 using hr::kLevels;
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+constexpr int kOverlapArena = 40 * 1024;  // solver shared arena when it runs beside the histograms
 
 // count a successful kernel launch
 inline cudaError_t counted(hr_ctx* c, cudaError_t e) {
@@ -196,6 +200,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_FUSED_BANDS")) c->fused_bands = atoi(v) > 0 ? atoi(v) : 2;
   if (const char* v = getenv("HR_FUSED_GS")) c->fused_gs = atoi(v) > 0 ? atoi(v) : 8;
   if (const char* v = getenv("HR_SOLVE_CPSM")) c->solve_cpsm = atoi(v) >= 0 && atoi(v) <= 2 ? atoi(v) : 0;
+  if (const char* v = getenv("HR_HIST_OVERLAP")) c->hist_overlap = atoi(v) != 0;
   *out = c;
   return HR_OK;
 }
@@ -241,7 +246,7 @@ hr_status hr_set_policy(hr_ctx* c, const char* key, int64_t v) {
       {"fused_bands", &c->fused_bands, 1, 1 << 20}, {"fused_gs", &c->fused_gs, 1, 1 << 30},
       {"chunks", &c->chunks, 1, 1 << 16},           {"hist_cpsm", &c->hist_cpsm, 1, 2},
       {"apply_cpsm", &c->apply_cpsm, 1, 2},         {"warp_solver", &c->warp_solver, 0, 1},
-      {"solve_cpsm", &c->solve_cpsm, 0, 2},
+      {"solve_cpsm", &c->solve_cpsm, 0, 2},         {"hist_overlap", &c->hist_overlap, 0, 1},
   };
   for (const Knob& k : knobs) {
     if (strcmp(k.name, key) != 0) continue;
@@ -411,9 +416,14 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     if (r == cudaSuccess) r = counted(c, hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, hist_grid(c), s));
     return r;
   };
-  auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, uint32_t* ready = nullptr) -> cudaError_t {
+  auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, uint32_t* ready = nullptr,
+                         const uint32_t* hist_done = nullptr, int hist_bands = 0) -> cudaError_t {
     hr::SolveArgs a{};
     a.ready = c->warp_solver ? nullptr : ready;
+    a.hist_done = c->warp_solver ? nullptr : hist_done;
+    a.hist_grid = hist_bands;  // the histogram kernel's (clamped) grid
+    a.hist_H = H;
+    a.arena_bytes = hist_done ? kOverlapArena : 0;  // fits beside two histogram CTAs
     a.idx1_tab = tab;
     a.hist_s = hs + b0 * kLevels;
     a.hist_g = nullptr;
@@ -432,7 +442,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       return r;
     }
     a.lut = lut + b0 * kLevels;  // CDF + LUT tail fused into the solver CTA (no target round trip)
-    return counted(c, hr::launch_solve(a, nb, solve_cpsm_for(c, nb), s));
+    return counted(c, hr::launch_solve(a, nb, hist_done ? 2 : solve_cpsm_for(c, nb), s));
   };
   auto apply_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, const uint32_t* ready = nullptr) -> cudaError_t {
     return counted(c, hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s,
@@ -504,10 +514,17 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       if (e == cudaSuccess)
         e = counted(c, hr::launch_zero((char*)ws + z0, align_up(L.ctl + hr::fused_ctl_bytes(B)) - z0, st));
     }
+    // histograms at 2 x 256 threads per SM counting flushed segments per image: each solver CTA
+    // (beside them) starts once its image is complete (needs the zeroed control block)
+    const bool overlap = c->hist_overlap && ready && !c->warp_solver;
+    uint32_t* ctl = reinterpret_cast<uint32_t*>((char*)ws + L.ctl);
+    const int HG = hr::hist_grid_clamped(B, H, 2 * c->num_sms);
     if (e == cudaSuccess)
-      e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st));
+      e = overlap ? counted(c, hr::launch_hist(in, B, H, W, hs, graw, HG, st, 256, ctl + hr::kCtlHeader))
+                  : counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st));
     if (e == cudaSuccess) e = mark(1);
-    if (e == cudaSuccess) e = solve_chunk(0, B, st, ready);
+    if (e == cudaSuccess) e = overlap ? solve_chunk(0, B, st, ready, ctl + hr::kCtlHeader, HG)
+                                      : solve_chunk(0, B, st, ready);
     if (e == cudaSuccess) e = mark(2);
     if (e == cudaSuccess) e = apply_chunk(0, B, st, ready);
     if (e == cudaSuccess) e = mark(3);

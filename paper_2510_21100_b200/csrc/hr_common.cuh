@@ -71,10 +71,22 @@ constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kApplyThreads = 256;
 
 // Launch helpers implemented in the kernel translation units.
+// nt: threads per CTA (512, or 256 to leave room for a solver CTA); done (nullable): per-image
+// counts of flushed segments (see hist_segments_of)
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
-                        uint32_t* hist_graw, int grid, cudaStream_t st);
+                        uint32_t* hist_graw, int grid, cudaStream_t st, int nt = kHistThreads,
+                        uint32_t* done = nullptr);
+int hist_grid_clamped(int64_t B, int32_t H, int grid);  // the grid launch_hist actually uses
+// number of k_hist CTA row ranges [R c / G, R (c+1) / G) overlapping image b's rows [bH, (b+1)H)
+__host__ __device__ inline int hist_segments_of(int64_t b, int64_t H, int64_t R, int64_t G) {
+  const int64_t first = ((b * H + 1) * G + R - 1) / R - 1;      // min c with R (c+1) / G > bH
+  int64_t last = ((b + 1) * H * G + R - 1) / R - 1;             // max c with R c / G < (b+1) H
+  if (last > G - 1) last = G - 1;
+  return (int)(last - first + 1);
+}
 cudaError_t launch_remap(const uint32_t* hist_graw, int64_t B, int32_t grad_norm, uint32_t* hist_g,
                          cudaStream_t st);
+
 
 struct SolveArgs {
   const uint32_t* hist_s;   // [B][256]
@@ -92,12 +104,16 @@ struct SolveArgs {
   const uint8_t* idx1_tab;  // [256][256] index_1(i, j) for params.gamma (launch_idx1_table)
   const int32_t* only_deferred;  // k_solve: when set, images with only_deferred[b] == 0 are skipped
   uint32_t* ready;               // [B] nullable (k_solve): released (= 1) once image b's LUT is written
+  const uint32_t* hist_done;     // [B] nullable (k_solve): start image b once all its segments flushed
+  int32_t hist_grid;             // ... k_hist's grid (the segment count follows from it)
+  int32_t hist_H;                // ... rows per image
+  int32_t arena_bytes;           // shared run arena per CTA (0: the default 80 KB)
 };
 // warp-per-image solver for nR <= 32; flags the other images in deferred[b] (then run k_solve)
 cudaError_t launch_solve_warp(const SolveArgs& a, int64_t B, int32_t* deferred, cudaStream_t st);
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st);
 cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t st);
-size_t solve_smem_bytes();
+size_t solve_smem_bytes(int arena_bytes = 0);
 size_t solve_cells_ws_bytes(int64_t B);
 
 cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,

@@ -13,8 +13,22 @@ namespace {
 __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int wscr[NW];
-  pdl_wait();
-  pdl_trigger();
+  if (args.hist_done) {  // overlap the histogram pass: wait for this image's segments only
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+      const int64_t Bn = gridDim.x, H = args.hist_H;
+      const uint32_t need = (uint32_t)hist_segments_of(blockIdx.x, H, Bn * H, args.hist_grid);
+      long long spins = 0;
+      while (ld_acquire(args.hist_done + blockIdx.x) < need) {
+        __nanosleep(256);
+        if (++spins > (1LL << 25)) asm volatile("trap;");  // ~10 s: a logic error, not a wait
+      }
+    }
+    __syncthreads();
+  } else {
+    pdl_wait();
+    pdl_trigger();
+  }
   solve_image(args, blockIdx.x, smraw, wscr);
   if (args.ready) {  // every exit of solve_image arrives here: LUT written -> release ready[b]
     __threadfence();
@@ -57,7 +71,7 @@ __global__ void __launch_bounds__(T) k_match(const uint32_t* hist_s, const doubl
 
 }  // namespace
 
-size_t solve_smem_bytes() { return sizeof(Sm) + (size_t)kArenaSmem; }
+size_t solve_smem_bytes(int arena_bytes) { return sizeof(Sm) + (size_t)(arena_bytes > 0 ? arena_bytes : kArenaSmem); }
 size_t solve_cells_ws_bytes(int64_t B) { return (size_t)B * (size_t)kArenaGlobal; }
 
 // cpsm == 1: request enough shared memory that only one solver CTA fits on an SM (the CTA
@@ -71,7 +85,7 @@ cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t s
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const size_t smem = cpsm == 1 ? std::max(solve_smem_bytes(), kOnePerSm) : solve_smem_bytes();
+  const size_t smem = cpsm == 1 ? std::max(solve_smem_bytes(a.arena_bytes), kOnePerSm) : solve_smem_bytes(a.arena_bytes);
   return launch_pdl(k_solve, dim3((unsigned)B), dim3(T), smem, st, a);
 }
 

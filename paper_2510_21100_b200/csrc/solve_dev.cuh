@@ -52,10 +52,10 @@ constexpr int kPiece = 8;
 constexpr int kMaxRuns = 32896;                        // sum_{i<256} (i + 1): runs of any image
 constexpr int kMaxPieces = kMaxRuns + 65536 / kPiece;  // P <= RR + E / kPiece
 constexpr int kMaskBytes = kLevels * 8 * 4;            // per-bin row bitmask (8 words per bin)
-constexpr int kArenaSmem = 80 * 1024;                  // keys (E bytes) + run arena + mask tail
-constexpr int kArenaGlobal = 12 * kMaxPieces + 256;  // arena when smem is short
+constexpr int kArenaSmem = 80 * 1024;  // default shared arena: keys (E bytes) + run arena + mask tail
+constexpr int kKeysGlobal = 65536;      // keys of images whose keys do not fit the shared arena
+constexpr int kArenaGlobal = 12 * kMaxPieces + 256 + kKeysGlobal;  // per-image global arena
 static_assert(8 * kMaxPieces >= 8 * kMaxRuns, "build scratch must fit under pVal");
-static_assert(kArenaSmem >= 65536 + kMaskBytes, "keys of the largest image must fit in smem");
 
 // Phase clock marks (measurement builds only: -DHR_SOLVE_PROFILE; block kProfBlock, thread 0).
 #ifdef HR_SOLVE_PROFILE
@@ -284,7 +284,7 @@ struct RunArena {
 // scan of the per-slot piece counts places every piece in bin order.  Placement: after the
 // keys in shared memory when it fits (mask tail excluded), else arenaG.
 __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* mask, unsigned char* arenaS,
-                          unsigned char* arenaG, RunArena& A, int* wscr) {
+                          int arenaBytes, bool keysInSmem, unsigned char* arenaG, RunArena& A, int* wscr) {
   const int tid = threadIdx.x;
   const int E = nR * nL;
   for (int i = tid; i < kLevels * 8; i += T) mask[i] = 0u;
@@ -303,8 +303,9 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   int RR;
   int r = block_scan_excl(cnt, &RR, wscr);
   const int Pmax = RR + E / kPiece;
-  const bool sm = align16(E) + align16(4 * Pmax) + 8 * Pmax <= kArenaSmem - kMaskBytes;
-  unsigned char* base = sm ? arenaS + align16(E) : arenaG;
+  const int keysS = keysInSmem ? align16(E) : 0;
+  const bool sm = keysS + align16(4 * Pmax) + 8 * Pmax <= arenaBytes - kMaskBytes;
+  unsigned char* base = sm ? arenaS + keysS : arenaG;
   A.pDesc = reinterpret_cast<uint32_t*>(base);
   A.pVal = reinterpret_cast<double*>(base + align16(4 * Pmax));
   A.RR = RR;
@@ -567,7 +568,8 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   Sm& s = *reinterpret_cast<Sm*>(smraw);
   unsigned char* arenaS = smraw + sizeof(Sm);
   // shared arena: [ keys (E bytes) | run arena (when it fits) | ... | mask 8 KB ]
-  uint32_t* mask = reinterpret_cast<uint32_t*>(arenaS + kArenaSmem - kMaskBytes);
+  const int AB = args.arena_bytes > 0 ? args.arena_bytes : kArenaSmem;
+  uint32_t* mask = reinterpret_cast<uint32_t*>(arenaS + AB - kMaskBytes);
   const int tid = threadIdx.x;
   const hr_params& P = args.p;
   if (args.only_deferred && args.only_deferred[b] == 0) return;  // solved by k_solve_warp
@@ -629,17 +631,19 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   }
 
   // ---- runs of index(i,j) along each compacted row (fixed for all t) ----
-  // keys kc (u8 per cell, always fits: E <= 65536 <= arena - mask) at the arena start
+  // keys kc (u8 per cell) at the shared arena start, or at the end of the global arena when
+  // E does not fit (only with a reduced shared arena: the default holds E = 65536)
   const int E = nR * nL;
-  uint8_t* kc = arenaS;
+  unsigned char* arenaG = args.cells_ws + b * (int64_t)kArenaGlobal;
+  const bool keysS = E <= AB - kMaskBytes;
+  uint8_t* kc = keysS ? arenaS : arenaG + (kArenaGlobal - kKeysGlobal);
   for (int e = tid; e < E; e += T) {
     const int a = e / nL, c = e - a * nL;
     kc[e] = (uint8_t)idx0(s.listR[a], s.listL[c]);
   }
   __syncthreads();
-  unsigned char* arenaG = args.cells_ws + b * (int64_t)kArenaGlobal;
   RunArena A;
-  run_build(s, nR, nL, kc, mask, arenaS, arenaG, A, wscr);
+  run_build(s, nR, nL, kc, mask, arenaS, AB, keysS, arenaG, A, wscr);
   PROF_MARK();
 
   const int t = iterate(s, P, nR, nL, N, kc, A);
@@ -652,13 +656,13 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
 
   // ---- Eq. 20: runs of index_1 (Eqs. 17-19) along each row, summed per bin in row order ----
   // index_1 of every cell from the per-gamma table (built once per gamma by k_idx1_table)
-  uint8_t* kc1 = arenaS;
+  uint8_t* kc1 = kc;
   for (int e = tid; e < E; e += T) {
     const int a = e / nL, c = e - a * nL;
     kc1[e] = __ldg(args.idx1_tab + s.listR[a] * kLevels + s.listL[c]);
   }
   __syncthreads();
-  run_build(s, nR, nL, kc1, mask, arenaS, arenaG, A, wscr);
+  run_build(s, nR, nL, kc1, mask, arenaS, AB, keysS, arenaG, A, wscr);
   for (int p = tid; p < A.P; p += T) {  // piece values hR_a * sum(hL over the piece)
     const uint32_t d = A.pDesc[p];
     const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;

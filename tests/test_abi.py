@@ -126,3 +126,43 @@ def test_python_binding_fails_loudly_without_cuda():
     x = torch.zeros((1, 4, 4, 3), dtype=torch.uint8)  # CPU tensor
     with pytest.raises(ValueError, match="CUDA"):
         hr.hr_enhance(x)
+
+
+def test_hist_segments_of_bruteforce(tmp_path):
+    """hist_segments_of (hr_common.cuh) = the number of k_hist CTA row ranges
+    [R c / G, R (c+1) / G) overlapping image b, by brute force over many (B, H, G).  k_solve
+    waits for exactly that many flushed segments, so an error here is a hang or a race."""
+    import shutil
+    import subprocess
+
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    src = tmp_path / "seg.cu"
+    src.write_text(r'''
+#include "hr_common.cuh"
+#include <cstdio>
+int main() {
+  long bad = 0, n = 0;
+  for (long B : {1L, 2L, 3L, 7L, 64L, 256L})
+    for (long H : {1L, 2L, 5L, 37L, 400L, 1080L})
+      for (long G : {1L, 2L, 7L, 148L, 296L, 1000L}) {
+        const long R = B * H;
+        if (G > R) continue;  // launch_hist clamps the grid to the rows
+        for (long b = 0; b < B; ++b) {
+          int cnt = 0;
+          for (long c = 0; c < G; ++c) {
+            const long r0 = R * c / G, r1 = R * (c + 1) / G;
+            if (r0 < (b + 1) * H && r1 > b * H) ++cnt;
+          }
+          ++n;
+          if (cnt != hr::hist_segments_of(b, H, R, G)) ++bad;
+        }
+      }
+  printf("%ld %ld\n", n, bad);
+  return 0;
+}
+''')
+    inc = os.path.join(ROOT, "paper_2510_21100_b200", "csrc")
+    exe = tmp_path / "seg"
+    subprocess.check_call([nvcc, "-std=c++17", "-I", inc, "-o", str(exe), str(src)])
+    n, bad = map(int, subprocess.check_output([str(exe)]).split())
+    assert n > 1000 and bad == 0
