@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhistretinex.so")
+# HR_LIB selects another build of the same library (e.g. the checked build in tools/)
+LIB_PATH = os.environ.get("HR_LIB") or os.path.join(HERE, "libhistretinex.so")
 
 HR_OK, HR_EINVAL, HR_EEMPTY, HR_EDEGENERATE, HR_ECUDA, HR_EUNSUPPORTED = range(6)
 

@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <utility>
@@ -11,6 +12,24 @@
 #include "../../include/histretinex.h"
 
 namespace hr {
+
+// ---- invariant checks (checked builds only: -DHR_CHECKS; tools/build_measure_libs.sh) ----
+// compute-sanitizer is not available on the GPU pool, so a checked build asserts the indexing
+// invariants the kernels rely on and the whole GPU suite runs against it (HR_LIB=...).
+#ifdef HR_CHECKS
+#define HR_CHECK(cond)                                                                       \
+  do {                                                                                       \
+    if (!(cond)) {                                                                           \
+      printf("HR_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                             \
+      asm volatile("trap;");                                                                 \
+    }                                                                                        \
+  } while (0)
+#else
+#define HR_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
 
 // ---- programmatic dependent launch (PDL) ----
 // Kernels of a step are launched with programmatic stream serialization: a kernel's launch

@@ -105,6 +105,7 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
       if (i >= 2) bulk_wait_read<1>();
       issue(i + kAhead);
     }
+    HR_CHECK(bytes > 0 && bytes <= (uint32_t)kChunkBytes && bytes % 48 == 0 && off + bytes <= (uint64_t)B * HW * 3);
     mbar_wait(&s.bar[w][st], ph);
     uint8_t* p = s.stage[w][st];
     apply_chunk_smem(p, bytes, tab, lane);

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(kFT, 2) k_fused(const FusedArgs a) {
     uint32_t bimg, bytes;
     uint64_t off;
     locate(c, bimg, off, bytes);
+    HR_CHECK(c < total && bimg < a.B && bytes > 0 && bytes <= (uint32_t)kChunkBytes);
     if ((int64_t)bimg != cur_img) {  // image switch: rebuild the per-warp (e, M) table
       __syncwarp();
       if (bimg == pend_img) {

@@ -303,6 +303,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   int RR;
   int r = block_scan_excl(cnt, &RR, wscr);
   const int Pmax = RR + E / kPiece;
+  HR_CHECK(RR >= nR && RR <= E && RR <= kMaxRuns);
   const int keysS = keysInSmem ? align16(E) : 0;
   const bool sm = keysS + align16(4 * Pmax) + 8 * Pmax <= arenaBytes - kMaskBytes;
   unsigned char* base = sm ? arenaS + keysS : arenaG;
@@ -349,6 +350,8 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   for (int q = r0; q < r1; ++q) {  // piece count at the run's bin-order slot
     const uint32_t d = runDesc[q];
     const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
+    HR_CHECK(lo <= hi && hi < nL && a < nR);
+    HR_CHECK(s.keyStart[k] + mask_rank(mask + k * 8, a) < RR);
     slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)] = (uint32_t)((hi - lo) / kPiece + 1);
   }
   __syncthreads();
@@ -362,6 +365,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     off += n;
   }
   A.P = P;
+  HR_CHECK(P >= RR && P <= Pmax && RK == RR);
   __syncthreads();
   for (int q = r0; q < r1; ++q) {  // pieces of each run at its bin-order offset
     const uint32_t d = runDesc[q];
@@ -369,6 +373,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     int p = (int)slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)];
     for (int l = lo; l <= hi; l += kPiece, ++p)
       A.pDesc[p] = (uint32_t)l | ((uint32_t)min(l + kPiece - 1, hi) << 8) | ((uint32_t)a << 16);
+    HR_CHECK(p <= P);
   }
   __syncthreads();
   s.keyStart[tid] = kfirst < RK ? (int)slotN[kfirst] : P;  // run slots -> piece offsets
