@@ -115,6 +115,19 @@ hr_status hr_solve(hr_ctx* ctx, const uint32_t* hist_s_dev, const uint32_t* hist
                    const hr_params* params, double* hL_dev, double* hR_dev, double* target_dev,
                    int32_t* iters_dev, void* ws_dev, void* stream);
 
+/* hr_solve with the Eq. 10 objective trace (diagnostics):
+   three values per update t, K frozen at the state of update t (Eq. 11):
+   trace[b][3t]   = F(hR^t,  hL^t),   before Eq. 13
+   trace[b][3t+1] = F(hR',   hL^t),   after Eq. 13 (raw, before renormalisation)
+   trace[b][3t+2] = F(hR',   hL'),    after Eq. 12 (raw)
+   F = sum_ij (hR_i hL_j / N - K_ij hS_index(i,j))^2 + alpha |hL - hS|^2 + beta |hR - hG|^2.
+   trace_dev: double [B][trace_stride], trace_stride >= 3 * params->max_iter; entries from
+   3 * iters on are zero.  Slower than hr_solve (one more pass over the cells per value). */
+hr_status hr_solve_trace(hr_ctx* ctx, const uint32_t* hist_s_dev, const uint32_t* hist_g_dev, int64_t B,
+                         const hr_params* params, double* hL_dev, double* hR_dev, double* target_dev,
+                         int32_t* iters_dev, double* trace_dev, int32_t trace_stride, void* ws_dev,
+                         void* stream);
+
 /* Step (3): histogram matching (R16).  Cs(v) = Ps(v)/N with Ps the integer prefix
    of hist_s; Pt(k) = Pt(k-1) + target(k) (plateau-preserving), Ct(k) = Pt(k)/Pt(255);
    lut[b][v] = smallest k minimising |Ct(k) - Cs(v)| (monotone non-decreasing in v).

@@ -23,7 +23,7 @@ from ._lib import HrError
 
 __all__ = ["Params", "HrError", "hr_histogram", "hr_solve", "hr_match", "hr_apply", "hr_enhance",
            "hr_enhance_debug", "workspace_bytes", "version", "profile_enable", "profile_collect",
-           "set_policy", "kernel_launches", "hr_enhance_host", "last_path"]
+           "set_policy", "kernel_launches", "hr_enhance_host", "last_path", "hr_solve_trace"]
 
 
 @dataclass
@@ -139,6 +139,28 @@ def hr_solve(hist_s: torch.Tensor, hist_g: torch.Tensor, params: Params | None =
     _check(_lib.load().hr_solve(ctx, _ptr(hist_s), _ptr(hist_g), B, ctypes.byref(pc), _ptr(hL), _ptr(hR),
                                 _ptr(tg), _ptr(it), _ptr(ws), _stream(dev)), ctx)
     return hL, hR, tg, it
+
+
+def hr_solve_trace(hist_s: torch.Tensor, hist_g: torch.Tensor, params: Params | None = None):
+    """hr_solve plus the Eq. 10 objective trace (3 values per update, K frozen).  Returns
+    (hL, hR, target, iters, trace) with trace float64 [B, 3 * max_iter]."""
+    p = params or Params()
+    _cuda(hist_s, torch.int32, "hist_s")
+    _cuda(hist_g, torch.int32, "hist_g")
+    B = hist_s.shape[0]
+    dev = hist_s.device
+    hL = torch.empty((B, 256), dtype=torch.float64, device=dev)
+    hR = torch.empty_like(hL)
+    tg = torch.empty_like(hL)
+    it = torch.empty((B,), dtype=torch.int32, device=dev)
+    stride = 3 * p.max_iter
+    tr = torch.empty((B, stride), dtype=torch.float64, device=dev)
+    pc = p.c()
+    ws = _workspace(B, 1, 1, dev)
+    ctx = _context(dev)
+    _check(_lib.load().hr_solve_trace(ctx, _ptr(hist_s), _ptr(hist_g), B, ctypes.byref(pc), _ptr(hL), _ptr(hR),
+                                      _ptr(tg), _ptr(it), _ptr(tr), stride, _ptr(ws), _stream(dev)), ctx)
+    return hL, hR, tg, it, tr
 
 
 def hr_match(hist_s: torch.Tensor, target: torch.Tensor):

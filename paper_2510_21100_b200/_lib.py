@@ -19,7 +19,7 @@ EXPORTS = (
     "hr_default_params", "hr_create", "hr_destroy", "hr_status_string", "hr_last_error",
     "hr_version", "hr_workspace_bytes", "hr_histogram", "hr_solve", "hr_match", "hr_apply",
     "hr_enhance", "hr_enhance_debug", "hr_profile_enable", "hr_profile_collect", "hr_set_policy",
-    "hr_kernel_launches", "hr_enhance_host", "hr_last_path",
+    "hr_kernel_launches", "hr_enhance_host", "hr_last_path", "hr_solve_trace",
 )
 
 
@@ -71,6 +71,7 @@ def load() -> ctypes.CDLL:
         "hr_workspace_bytes": ([i64, i32, i32], sz),
         "hr_histogram": ([vp, vp, i64, i32, i32, i32, vp, vp, vp, vp, vp], i32),
         "hr_solve": ([vp, vp, vp, i64, P, vp, vp, vp, vp, vp, vp], i32),
+        "hr_solve_trace": ([vp, vp, vp, i64, P, vp, vp, vp, vp, vp, i32, vp, vp], i32),
         "hr_match": ([vp, vp, vp, i64, vp, vp, vp], i32),
         "hr_apply": ([vp, vp, vp, i64, i32, i32, vp, vp], i32),
         "hr_enhance": ([vp, vp, i64, i32, i32, P, vp, vp, vp], i32),

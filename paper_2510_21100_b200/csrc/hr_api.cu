@@ -320,8 +320,9 @@ hr_status hr_histogram(hr_ctx* c, const uint8_t* rgb, int64_t B, int32_t H, int3
   return cuda_err(c, e, "hr_histogram");
 }
 
-hr_status hr_solve(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, int64_t B, const hr_params* p,
-                   double* hL, double* hR, double* target, int32_t* iters, void* ws, void* stream) {
+static hr_status solve_impl(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, int64_t B, const hr_params* p,
+                            double* hL, double* hR, double* target, int32_t* iters, double* trace,
+                            int32_t trace_stride, void* ws, void* stream) {
   if (!c) return HR_EINVAL;
   if (!hist_s || !hist_g || !hL || !hR || !target || !ws) return set_err(c, HR_EINVAL, "NULL pointer");
   if (B < 1 || B > (1 << 30)) return set_err(c, HR_EINVAL, "B must be >= 1");
@@ -346,13 +347,29 @@ hr_status hr_solve(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, in
   a.iters = iters;
   a.lut = nullptr;
   a.status = nullptr;
+  a.trace = trace;
+  a.trace_stride = trace_stride;
   cudaError_t e = cudaSuccess;
-  if (c->warp_solver) {
+  if (c->warp_solver && !trace) {  // (the warp solver has no objective trace)
     e = counted(c, hr::launch_solve_warp(a, B, deferred, (cudaStream_t)stream));
     a.only_deferred = deferred;
   }
   if (e == cudaSuccess) e = counted(c, hr::launch_solve(a, B, solve_cpsm_for(c, B), (cudaStream_t)stream));
-  return cuda_err(c, e, "hr_solve");
+  return cuda_err(c, e, trace ? "hr_solve_trace" : "hr_solve");
+}
+
+hr_status hr_solve(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, int64_t B, const hr_params* p,
+                   double* hL, double* hR, double* target, int32_t* iters, void* ws, void* stream) {
+  return solve_impl(c, hist_s, hist_g, B, p, hL, hR, target, iters, nullptr, 0, ws, stream);
+}
+
+hr_status hr_solve_trace(hr_ctx* c, const uint32_t* hist_s, const uint32_t* hist_g, int64_t B, const hr_params* p,
+                         double* hL, double* hR, double* target, int32_t* iters, double* trace,
+                         int32_t trace_stride, void* ws, void* stream) {
+  if (!c) return HR_EINVAL;
+  if (!trace) return set_err(c, HR_EINVAL, "NULL trace");
+  if (p && trace_stride < 3 * p->max_iter) return set_err(c, HR_EINVAL, "trace_stride < 3 * max_iter");
+  return solve_impl(c, hist_s, hist_g, B, p, hL, hR, target, iters, trace, trace_stride, ws, stream);
 }
 
 hr_status hr_match(hr_ctx* c, const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,

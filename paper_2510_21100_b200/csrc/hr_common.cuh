@@ -127,6 +127,8 @@ struct SolveArgs {
   int32_t hist_grid;             // ... k_hist's grid (the segment count follows from it)
   int32_t hist_H;                // ... rows per image
   int32_t arena_bytes;           // shared run arena per CTA (0: the default 80 KB)
+  double* trace;                 // [B][trace_stride] nullable: Eq. 10 objective, 3 values per update
+  int32_t trace_stride;
 };
 // warp-per-image solver for nR <= 32; flags the other images in deferred[b] (then run k_solve)
 cudaError_t launch_solve_warp(const SolveArgs& a, int64_t B, int32_t* deferred, cudaStream_t st);

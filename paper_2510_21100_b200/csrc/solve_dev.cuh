@@ -77,7 +77,7 @@ constexpr int kProfBlock = 0;
 #endif
 
 // slots of the block-reduction scratch
-enum { R_SL2 = 0, R_SR1, R_SR2, R_SL1, R_DR, R_DL, R_QL1, kSlots };
+enum { R_SL2 = 0, R_SR1, R_SR2, R_SL1, R_DR, R_DL, R_QL1, R_OBJ, kSlots };
 
 struct __align__(16) Sm {
   double hR[kLevels], hL[kLevels];    // renormalised state (index a over sR, c over sL)
@@ -414,6 +414,37 @@ __device__ __forceinline__ double rcp_fast(double x) {
   return fma(r, e, r);
 }
 
+// Eq. 10 objective with K frozen at the current state (s.hR, s.hL, rho of this
+// update): F = sum_cells (X_a Y_c / N - K_ac hS_k)^2 + alpha sum (Y - hS)^2 + beta sum (X - hG)^2,
+// K_ac hS_k = hR_a hL_c hS_k / EstRaw_k (Eq. 11); X, Y the evaluated reflectance / illumination.
+// Cells off the supports contribute 0.  Diagnostics only (hr_solve_trace): one more pass over the
+// cells and one block reduction per value; every thread returns the total.
+__device__ double objective(Sm& s, const hr_params& P, int nR, int nL, double N, const uint8_t* kc,
+                            const double* X, const double* Y) {
+  const int tid = threadIdx.x;
+  double acc = 0.0;
+  for (int e = tid; e < nR * nL; e += T) {
+    const int a = e / nL, c = e - a * nL, k = kc[e];
+    const double hsk = s.hSd[k];
+    const double rho = P.update_form == 0 ? s.rho[k] : (s.rho[k] > 0.0 ? hsk * hsk / s.rho[k] : 0.0);
+    const double r = X[a] * Y[c] / N - s.hR[a] * s.hL[c] * rho;
+    acc = fma(r, r, acc);
+  }
+  if (tid < nL) {
+    const double dl = Y[tid] - s.hSc[tid];
+    acc += P.alpha * dl * dl;
+  }
+  if (tid < nR) {
+    const double dr = X[tid] - s.hGc[tid];
+    acc += P.beta * dr * dr;
+  }
+  slot_put3(s, R_OBJ, acc, -1, 0.0, -1, 0.0);
+  __syncthreads();
+  const double F = slot_sum(s, R_OBJ);
+  __syncthreads();
+  return F;
+}
+
 // Algorithm 1 iterations over the run arena A.  Returns t.
 // Four phases per update, each closed by a barrier:
 //   E1  renormalise the raw iterates of the previous update (Eqs. 15, 14) and, one thread per
@@ -422,7 +453,7 @@ __device__ __forceinline__ double rcp_fast(double x) {
 //   R   TPR threads per row: A_a over the row's cells (cached keys kc), Eq. 13
 //   L   TPC threads per column: B_c over the rows, Eq. 12 with the frozen K
 __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL, double N, const uint8_t* kc,
-                                       const RunArena& A) {
+                                       const RunArena& A, double* trace = nullptr, int trace_cap = 0) {
   const int tid = threadIdx.x;
   // threads per row (R) / per column (L): the largest power of two with all rows / columns
   // covered by the T threads; each group sums its cells in a fixed order (deterministic)
@@ -484,6 +515,10 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
     const double invDenR = rcp_fast((t == 0 ? slot_sum(s, R_SL2) : cL * cL * QL1) * invN2 + P.beta);
     __syncthreads();
     PHASE(1);
+    if (trace) {  // before Eq. 13
+      const double F = objective(s, P, nR, nL, N, kc, s.hR, s.hL);
+      if (tid == 0 && 3 * t < trace_cap) trace[3 * t] = F;
+    }
     // ======== R: Eq. 13, TPR threads per row walking every TPR-th cell, fixed-order reduce ========
     {
       double A0 = 0.0, A1 = 0.0;
@@ -520,6 +555,10 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
     }
     __syncthreads();
     PHASE(2);
+    if (trace) {  // after Eq. 13 (raw hR', current hL)
+      const double F = objective(s, P, nR, nL, N, kc, s.hR1, s.hL);
+      if (tid == 0 && 3 * t + 1 < trace_cap) trace[3 * t + 1] = F;
+    }
     // ======== L: Eq. 12 (frozen K), TPC threads per column over every TPC-th row ========
     {
       const double invDenL = rcp_fast(slot_sum(s, R_SR2) * invN2 + P.alpha);
@@ -548,6 +587,10 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
     }
     __syncthreads();
     PHASE(3);
+    if (trace) {  // after Eq. 12 (raw hR', raw hL')
+      const double F = objective(s, P, nR, nL, N, kc, s.hR1, s.hL1);
+      if (tid == 0 && 3 * t + 2 < trace_cap) trace[3 * t + 2] = F;
+    }
     ++t;
     SR1 = slot_sum(s, R_SR1);
     SL1 = slot_sum(s, R_SL1);
@@ -651,7 +694,10 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   run_build(s, nR, nL, kc, mask, arenaS, AB, keysS, arenaG, A, wscr);
   PROF_MARK();
 
-  const int t = iterate(s, P, nR, nL, N, kc, A);
+  double* tr = args.trace ? args.trace + b * (int64_t)args.trace_stride : nullptr;
+  const int t = iterate(s, P, nR, nL, N, kc, A, tr, args.trace_stride);
+  if (tr && tid == 0)
+    for (int i = 3 * t; i < args.trace_stride; ++i) tr[i] = 0.0;
   PROF_MARK();
 
   // ---- outputs hL, hR (dense, zero off support) ----

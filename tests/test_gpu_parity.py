@@ -331,3 +331,36 @@ def test_errors_are_raised():
     with pytest.raises(m.HrError) as e:
         m.hr_enhance(torch.zeros((1, 0, 5, 3), dtype=torch.uint8, device="cuda"))
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("pset", ["default", "paper_form", "eps_rule", "gamma5_beta01"])
+def test_solve_trace_vs_oracle(pset):
+    """hr_solve_trace: the Eq. 10 objective, 3 values per update with K
+    frozen, against the oracle's trace; the traced solve leaves every output bit-identical to
+    hr_solve; in the gradient-consistent form each update is the exact minimiser of the
+    objective in its variable (Eq. 13 / Eq. 12 with K frozen), so the trace never increases
+    within an update."""
+    hp, op = P(**PARAM_SETS[pset])
+    imgs = [synth.make_image(120, 160, seed=7), synth.make_config("C5", batch=1)[0][:200, :300],
+            synth.make_image(90, 70, seed=8, peak=0.4)]
+    hs_l, hg_l = [], []
+    for im in imgs:
+        r = oracle.enhance(im, op)
+        hs_l.append(r.hS.astype(np.int32))
+        hg_l.append(r.hG.astype(np.int32))
+    hs, hg = to_dev(np.stack(hs_l)), to_dev(np.stack(hg_l))
+    hL, hR, tg, it, tr = (t.cpu().numpy() for t in hr().hr_solve_trace(hs, hg, hp))
+    hL0, hR0, tg0, it0 = (t.cpu().numpy() for t in hr().hr_solve(hs, hg, hp))
+    assert np.array_equal(hL, hL0) and np.array_equal(hR, hR0) and np.array_equal(tg, tg0)
+    assert np.array_equal(it, it0)
+    for b in range(len(imgs)):
+        _, _, oit, otr = oracle.decompose(np.asarray(hs_l[b], np.float64), np.asarray(hg_l[b], np.float64), op,
+                                          trace_cap=3 * op.max_iter)
+        n = 3 * oit
+        assert it[b] == oit
+        assert np.all(tr[b, n:] == 0.0)
+        rel = np.abs(tr[b, :n] - otr[:n]) / np.maximum(np.abs(otr[:n]), 1e-300)
+        assert rel.max() <= 1e-9, (pset, b, rel.max())
+        if op.update_form == 0:
+            f = tr[b, :n].reshape(-1, 3)
+            assert np.all(f[:, 1] <= f[:, 0] * (1 + 1e-12)) and np.all(f[:, 2] <= f[:, 1] * (1 + 1e-12))
