@@ -78,6 +78,11 @@ def lib() -> ctypes.CDLL:
     if _lib is None:
         _lib = ctypes.CDLL(build())
         _lib.ho_objective.restype = ctypes.c_double
+        for f in ("ho_psnr", "ho_ssim", "ho_loe"):
+            getattr(_lib, f).restype = ctypes.c_double
+        _lib.ho_psnr.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+        _lib.ho_ssim.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
+        _lib.ho_loe.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
     return _lib
 
 
@@ -250,6 +255,33 @@ def reconstruct(rgb, Vnew) -> np.ndarray:
     out = np.empty_like(rgb)
     _ck(lib().ho_reconstruct(_p(rgb), ctypes.c_int64(rgb.size // 3), _p(Vnew), _p(out)), "reconstruct")
     return out
+
+
+# ------------------------------------------- second workload (NEXT #4): HE and metrics
+def he_enhance(rgb) -> np.ndarray:
+    """HE baseline (Eq. 5): V -> round(255 CDF(V)), colour by R17.  rgb [H, W, 3] uint8."""
+    rgb = _u8(rgb)
+    out = np.empty_like(rgb)
+    _ck(lib().ho_he_enhance(_p(rgb), rgb.shape[0], rgb.shape[1], _p(out)), "he_enhance")
+    return out
+
+
+def psnr(a, b) -> float:
+    a, b = _u8(a), _u8(b)
+    assert a.shape == b.shape
+    return float(lib().ho_psnr(_p(a), _p(b), a.size // 3))
+
+
+def ssim(a, b) -> float:
+    a, b = _u8(a), _u8(b)
+    assert a.shape == b.shape
+    return float(lib().ho_ssim(_p(a), _p(b), a.shape[0], a.shape[1]))
+
+
+def loe(orig, enh) -> float:
+    a, b = _u8(orig), _u8(enh)
+    assert a.shape == b.shape
+    return float(lib().ho_loe(_p(a), _p(b), a.shape[0], a.shape[1]))
 
 
 # ---------------------------------------------------------------- pipeline

@@ -691,3 +691,119 @@ int ho_enhance_batch(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, const 
   free(idx1);
   return J.rc;
 }
+
+/* ============================ second workload: HE baseline and quality metrics (NEXT #4) */
+
+int ho_he_enhance(const uint8_t* rgb, int32_t H, int32_t W, uint8_t* out) {
+  if (!rgb || !out || H <= 0 || W <= 0) return HO_EINVAL;
+  const int64_t n = (int64_t)H * W;
+  uint64_t hS[256];
+  int32_t t[256];
+  memset(hS, 0, sizeof hS);
+  for (int64_t p = 0; p < n; ++p) {
+    uint8_t v = rgb[3 * p];
+    if (rgb[3 * p + 1] > v) v = rgb[3 * p + 1];
+    if (rgb[3 * p + 2] > v) v = rgb[3 * p + 2];
+    hS[v]++;
+  }
+  int rc = ho_he_transform(hS, 256, t);
+  if (rc) return rc;
+  int32_t* Vn = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  if (!Vn) return HO_EINVAL;
+  for (int64_t p = 0; p < n; ++p) {
+    uint8_t v = rgb[3 * p];
+    if (rgb[3 * p + 1] > v) v = rgb[3 * p + 1];
+    if (rgb[3 * p + 2] > v) v = rgb[3 * p + 2];
+    Vn[p] = t[v];
+  }
+  rc = ho_reconstruct(rgb, n, Vn, out);
+  free(Vn);
+  return rc;
+}
+
+double ho_psnr(const uint8_t* a, const uint8_t* b, int64_t npix) {
+  uint64_t sse = 0;
+  for (int64_t i = 0; i < 3 * npix; ++i) {
+    const int64_t d = (int64_t)a[i] - (int64_t)b[i];
+    sse += (uint64_t)(d * d);
+  }
+  if (sse == 0) return INFINITY;
+  const double mse = (double)sse / (double)(3 * npix);
+  return 10.0 * log10(255.0 * 255.0 / mse);
+}
+
+double ho_ssim(const uint8_t* a, const uint8_t* b, int32_t H, int32_t W) {
+  if (H < 11 || W < 11) return NAN;
+  const int R = 5;
+  double g[11], gs = 0.0;
+  for (int k = -R; k <= R; ++k) {
+    g[k + R] = exp(-(double)(k * k) / (2.0 * 1.5 * 1.5));
+    gs += g[k + R];
+  }
+  for (int k = 0; k < 11; ++k) g[k] /= gs;
+  const double C1 = (0.01 * 255.0) * (0.01 * 255.0), C2 = (0.03 * 255.0) * (0.03 * 255.0);
+  const size_t n = (size_t)H * W;
+  double* ya = (double*)malloc(sizeof(double) * n);
+  double* yb = (double*)malloc(sizeof(double) * n);
+  if (!ya || !yb) {
+    free(ya);
+    free(yb);
+    return NAN;
+  }
+  for (size_t p = 0; p < n; ++p) {
+    ya[p] = 0.299 * a[3 * p] + 0.587 * a[3 * p + 1] + 0.114 * a[3 * p + 2];
+    yb[p] = 0.299 * b[3 * p] + 0.587 * b[3 * p + 1] + 0.114 * b[3 * p + 2];
+  }
+  double sum = 0.0;
+  for (int y = R; y < H - R; ++y)
+    for (int x = R; x < W - R; ++x) {
+      double ma = 0.0, mb = 0.0, saa = 0.0, sbb = 0.0, sab = 0.0;
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx) {
+          const double w = g[dy + R] * g[dx + R];
+          const size_t q = (size_t)(y + dy) * W + (x + dx);
+          ma += w * ya[q];
+          mb += w * yb[q];
+          saa += w * ya[q] * ya[q];
+          sbb += w * yb[q] * yb[q];
+          sab += w * ya[q] * yb[q];
+        }
+      const double va = saa - ma * ma, vb = sbb - mb * mb, cov = sab - ma * mb;
+      sum += ((2.0 * ma * mb + C1) * (2.0 * cov + C2)) / ((ma * ma + mb * mb + C1) * (va + vb + C2));
+    }
+  free(ya);
+  free(yb);
+  return sum / ((double)(H - 2 * R) * (double)(W - 2 * R));
+}
+
+double ho_loe(const uint8_t* orig, const uint8_t* enh, int32_t H, int32_t W) {
+  if (!orig || !enh || H <= 0 || W <= 0) return NAN;
+  const int mh = H < 100 ? H : 100, mw = W < 100 ? W : 100;
+  const int m = mh * mw;
+  uint8_t* L = (uint8_t*)malloc((size_t)m);
+  uint8_t* Le = (uint8_t*)malloc((size_t)m);
+  if (!L || !Le) {
+    free(L);
+    free(Le);
+    return NAN;
+  }
+  for (int i = 0; i < mh; ++i)
+    for (int j = 0; j < mw; ++j) {
+      const int64_t y = (int64_t)i * H / mh, x = (int64_t)j * W / mw;
+      const uint8_t* p = orig + 3 * (y * W + x);
+      const uint8_t* q = enh + 3 * (y * W + x);
+      uint8_t l = p[0], le = q[0];
+      if (p[1] > l) l = p[1];
+      if (p[2] > l) l = p[2];
+      if (q[1] > le) le = q[1];
+      if (q[2] > le) le = q[2];
+      L[i * mw + j] = l;
+      Le[i * mw + j] = le;
+    }
+  uint64_t cnt = 0;
+  for (int x = 0; x < m; ++x)
+    for (int y = 0; y < m; ++y) cnt += (uint64_t)((L[x] >= L[y]) != (Le[x] >= Le[y]));
+  free(L);
+  free(Le);
+  return (double)cnt / (double)m;
+}

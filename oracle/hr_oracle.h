@@ -131,6 +131,28 @@ int ho_enhance_batch(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, const 
                      uint8_t* out, uint64_t* hS, uint64_t* hG, double* hL, double* hR,
                      double* T, int32_t* lut, int32_t* iters, int32_t nthreads);
 
+/* ---------------------------------------------------------------------------------------
+   Second workload: the HE baseline and the quality metrics of §IV.
+   Definitions are SPEC.md's metrics module, which fixes what PAPER.md leaves
+   open (P:311 names PSNR [40], SSIM [41], LOE [15] without formulas).
+   --------------------------------------------------------------------------------------- */
+
+/* HE baseline (Eq. 5): V -> t_V with t from ho_he_transform, colour by R17. */
+int ho_he_enhance(const uint8_t* rgb, int32_t H, int32_t W, uint8_t* out);
+
+/* PSNR: 10 log10(255^2 / MSE), MSE over all three channels; identical -> +inf. */
+double ho_psnr(const uint8_t* a, const uint8_t* b, int64_t npix);
+
+/* SSIM: luma Y = 0.299 R + 0.587 G + 0.114 B; 11x11 Gaussian window, sigma 1.5,
+   normalised; valid windows only ((H-10) x (W-10) centres); C1 = (0.01*255)^2,
+   C2 = (0.03*255)^2; the mean of the SSIM map.  Needs H, W >= 11 (else NaN). */
+double ho_ssim(const uint8_t* a, const uint8_t* b, int32_t H, int32_t W);
+
+/* LOE: lightness L = max(R,G,B); both images sampled to mh x mw = min(H,100) x
+   min(W,100) by nearest neighbour (row i <- (i*H)/mh, column j <- (j*W)/mw); LOE =
+   (1/m) sum_x sum_y [(L(x) >= L(y)) xor (L'(x) >= L'(y))], m = mh * mw. */
+double ho_loe(const uint8_t* orig, const uint8_t* enh, int32_t H, int32_t W);
+
 #ifdef __cplusplus
 }
 #endif
