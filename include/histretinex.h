@@ -177,6 +177,30 @@ hr_status hr_enhance_debug(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, in
                            uint32_t* hist_s_dev, uint8_t* lut_dev, int32_t* iters_dev,
                            void* stream);
 
+/* ---- Second workload: the HE baseline and the quality metrics ---- */
+
+/* HE baseline (Eq. 5): V -> t_V = floor(255 c_V + 0.5), c the running sum of
+   hS_u / N (Eq. 4), with the R17 colour reconstruction of hr_apply.  lut_dev (nullable):
+   the [B][256] HE tables.  Workspace: hr_workspace_bytes(B, H, W).  rgb_out must not alias
+   rgb_in.  Bit-exact with the oracle. */
+hr_status hr_he(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H, int32_t W,
+                uint8_t* rgb_out_dev, uint8_t* lut_dev, void* ws_dev, void* stream);
+
+/* Bytes of device workspace hr_quality needs (0 for empty shapes). */
+size_t hr_quality_workspace_bytes(int64_t B, int32_t H, int32_t W);
+
+/* Quality metrics of image pairs a[b], b[b] (P:311 names them; SPEC.md metrics module defines
+   them): PSNR = 10 log10(255^2 / MSE) over all channels (+inf if equal); SSIM on luma
+   0.299R + 0.587G + 0.114B with an 11x11 Gaussian (sigma 1.5), valid windows, C1 = (0.01*255)^2,
+   C2 = (0.03*255)^2, the mean of the map (NaN if H or W < 11); LOE = (1/m) sum over pairs of
+   sampled pixels of [(L(x) >= L(y)) xor (L'(x) >= L'(y))], L = max(R,G,B) on a
+   min(H,100) x min(W,100) nearest-neighbour grid (row (i H)/mh, column (j W)/mw), a = original.
+   Outputs: double [B] each, nullable (at least one).  Workspace: hr_quality_workspace_bytes.
+   fp64; deterministic.  LOE is exact; PSNR and SSIM equal the oracle up to rounding order. */
+hr_status hr_quality(hr_ctx* ctx, const uint8_t* a_dev, const uint8_t* b_dev, int64_t B, int32_t H,
+                     int32_t W, double* psnr_dev, double* ssim_dev, double* loe_dev, void* ws_dev,
+                     void* stream);
+
 /* Stage timing (measurement only).  While enabled, every hr_enhance records four CUDA
    events on its stream.  Separate-kernel path: before the histogram kernel, after it,
    after the solver + LUT, after the apply kernel -> stage_ms[0] histogram incl. its

@@ -23,7 +23,8 @@ from ._lib import HrError
 
 __all__ = ["Params", "HrError", "hr_histogram", "hr_solve", "hr_match", "hr_apply", "hr_enhance",
            "hr_enhance_debug", "workspace_bytes", "version", "profile_enable", "profile_collect",
-           "set_policy", "kernel_launches", "hr_enhance_host", "last_path", "hr_solve_trace"]
+           "set_policy", "kernel_launches", "hr_enhance_host", "last_path", "hr_solve_trace", "hr_he",
+           "hr_quality"]
 
 
 @dataclass
@@ -260,6 +261,35 @@ def last_path(device=None) -> int:
     """hr_last_path: 0 separate kernels, 1 fused kernel, 2 chunk pipeline (last hr_enhance)."""
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     return int(_lib.load().hr_last_path(_context(dev)))
+
+
+def hr_he(rgb: torch.Tensor, out: torch.Tensor | None = None, return_lut: bool = False):
+    """HE baseline (Eq. 5) of a [B, H, W, 3] uint8 CUDA batch (SURVEY NEXT #4)."""
+    x = _images(rgb)
+    B, H, W, _ = x.shape
+    dev = x.device
+    out = torch.empty_like(x) if out is None else out
+    lut = torch.empty((B, 256), dtype=torch.uint8, device=dev)
+    ws = _workspace(B, H, W, dev)
+    ctx = _context(dev)
+    _check(_lib.load().hr_he(ctx, _ptr(x), B, H, W, _ptr(out), _ptr(lut), _ptr(ws), _stream(dev)), ctx)
+    return (out, lut) if return_lut else out
+
+
+def hr_quality(a: torch.Tensor, b: torch.Tensor):
+    """(psnr, ssim, loe) float64 [B] of image pairs (SPEC metrics; a = original for LOE)."""
+    x, y = _images(a), _images(b)
+    if x.shape != y.shape:
+        raise ValueError("a and b must have the same shape")
+    B, H, W, _ = x.shape
+    dev = x.device
+    ps = torch.empty((B,), dtype=torch.float64, device=dev)
+    ss, lo = torch.empty_like(ps), torch.empty_like(ps)
+    lib = _lib.load()
+    ws = torch.empty(max(1, lib.hr_quality_workspace_bytes(B, H, W)), dtype=torch.uint8, device=dev)
+    ctx = _context(dev)
+    _check(lib.hr_quality(ctx, _ptr(x), _ptr(y), B, H, W, _ptr(ps), _ptr(ss), _ptr(lo), _ptr(ws), _stream(dev)), ctx)
+    return ps, ss, lo
 
 
 def kernel_launches(device=None) -> int:

@@ -19,7 +19,8 @@ EXPORTS = (
     "hr_default_params", "hr_create", "hr_destroy", "hr_status_string", "hr_last_error",
     "hr_version", "hr_workspace_bytes", "hr_histogram", "hr_solve", "hr_match", "hr_apply",
     "hr_enhance", "hr_enhance_debug", "hr_profile_enable", "hr_profile_collect", "hr_set_policy",
-    "hr_kernel_launches", "hr_enhance_host", "hr_last_path", "hr_solve_trace",
+    "hr_kernel_launches", "hr_enhance_host", "hr_last_path", "hr_solve_trace", "hr_he",
+    "hr_quality_workspace_bytes", "hr_quality",
 )
 
 
@@ -82,6 +83,9 @@ def load() -> ctypes.CDLL:
         "hr_set_policy": ([vp, ctypes.c_char_p, i64], i32),
         "hr_kernel_launches": ([vp], i64),
         "hr_last_path": ([vp], i32),
+        "hr_he": ([vp, vp, i64, i32, i32, vp, vp, vp, vp], i32),
+        "hr_quality_workspace_bytes": ([i64, i32, i32], sz),
+        "hr_quality": ([vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

@@ -590,6 +590,43 @@ hr_status hr_enhance(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t
   return hr_enhance_debug(c, in, B, H, W, p, out, ws, nullptr, nullptr, nullptr, stream);
 }
 
+hr_status hr_he(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, uint8_t* out, uint8_t* lut_dbg,
+                void* ws, void* stream) {
+  if (!c) return HR_EINVAL;
+  hr_status s = check_shape(c, B, H, W);
+  if (s) return s;
+  if (!in || !out || !ws) return set_err(c, HR_EINVAL, "NULL pointer");
+  if (in == out) return set_err(c, HR_EINVAL, "rgb_out must not alias rgb_in");
+  if ((s = activate(c))) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const WsLayout L = ws_layout(B);
+  uint32_t* hs = reinterpret_cast<uint32_t*>((char*)ws + L.hist_s);
+  uint32_t* graw = reinterpret_cast<uint32_t*>((char*)ws + L.graw);
+  uint8_t* lut = lut_dbg ? lut_dbg : reinterpret_cast<uint8_t*>((char*)ws + L.lut);
+  cudaError_t e = counted(c, hr::launch_zero(hs, (size_t)B * kLevels * sizeof(uint32_t), st));
+  if (e == cudaSuccess) e = counted(c, hr::launch_zero(graw, (size_t)B * kGradSlots * sizeof(uint32_t), st));
+  if (e == cudaSuccess) e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st));
+  if (e == cudaSuccess) e = counted(c, hr::launch_he_lut(hs, B, lut, st));
+  if (e == cudaSuccess) e = counted(c, hr::launch_apply(in, lut, B, H, W, out, apply_grid(c), st));
+  return cuda_err(c, e, "hr_he");
+}
+
+size_t hr_quality_workspace_bytes(int64_t B, int32_t H, int32_t W) {
+  if (B <= 0 || H <= 0 || W <= 0) return 0;
+  return hr::quality_ws_bytes(B, H, W);
+}
+
+hr_status hr_quality(hr_ctx* c, const uint8_t* a, const uint8_t* b, int64_t B, int32_t H, int32_t W, double* psnr,
+                     double* ssim, double* loe, void* ws, void* stream) {
+  if (!c) return HR_EINVAL;
+  hr_status s = check_shape(c, B, H, W);
+  if (s) return s;
+  if (!a || !b || !ws) return set_err(c, HR_EINVAL, "NULL pointer");
+  if (!psnr && !ssim && !loe) return set_err(c, HR_EINVAL, "no metric requested");
+  if ((s = activate(c))) return s;
+  return cuda_err(c, hr::launch_quality(a, b, B, H, W, psnr, ssim, loe, ws, (cudaStream_t)stream), "hr_quality");
+}
+
 hr_status hr_enhance_host(hr_ctx* c, const uint8_t* in_h, int64_t B, int32_t H, int32_t W, const hr_params* p,
                           uint8_t* out_h, uint8_t* in_d, uint8_t* out_d, void* ws, int32_t chunks, void* stream) {
   if (!c) return HR_EINVAL;

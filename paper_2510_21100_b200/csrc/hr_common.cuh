@@ -144,6 +144,11 @@ cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B
 // does not wait for the solver grid to finish but acquires ready[b] before image b's table
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
                          uint8_t* out, int grid_ctas, cudaStream_t st, const uint32_t* ready = nullptr);
+// second workload (k_quality.cu): HE LUT per image (Eq. 4-5) and the quality metrics
+cudaError_t launch_he_lut(const uint32_t* hist_s, int64_t B, uint8_t* lut, cudaStream_t st);
+size_t quality_ws_bytes(int64_t B, int32_t H, int32_t W);
+cudaError_t launch_quality(const uint8_t* a, const uint8_t* b, int64_t B, int32_t H, int32_t W, double* psnr,
+                           double* ssim, double* loe, void* ws, cudaStream_t st);
 // zero n bytes (n % 16 == 0, 16-B aligned) -- replaces cudaMemsetAsync inside the PDL chain
 cudaError_t launch_zero(void* p, size_t n, cudaStream_t st);
 
