@@ -74,19 +74,22 @@ __global__ void __launch_bounds__(T) k_match(const uint32_t* hist_s, const doubl
 size_t solve_smem_bytes(int arena_bytes) { return sizeof(Sm) + (size_t)(arena_bytes > 0 ? arena_bytes : kArenaSmem); }
 size_t solve_cells_ws_bytes(int64_t B) { return (size_t)B * (size_t)kArenaGlobal; }
 
-// cpsm == 1: request enough shared memory that only one solver CTA fits on an SM (the CTA
-// scheduler would otherwise pack two latency-bound solves onto one SM while others idle).
-cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t st) {
-  constexpr size_t kOnePerSm = 120 * 1024;  // 2 x (120 KB + 1 KB reserved) > 228 KB per SM
+// cpsm == 1: one solver CTA per SM (the CTA scheduler would otherwise pack two latency-bound
+// solves onto one SM while others idle).  The shared memory that placement reserves anyway is
+// given to the run arena (kBigArena), so images with large supports (C4: E = 8480 cells) keep
+// their run structure in shared memory instead of the global arena.
+cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t st) {
+  constexpr int kBigArena = 190 * 1024;  // sizeof(Sm) + 190 KB <= 227 KB per block
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)std::max(solve_smem_bytes(), kOnePerSm));
+                                         (int)solve_smem_bytes(kBigArena));
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const size_t smem = cpsm == 1 ? std::max(solve_smem_bytes(a.arena_bytes), kOnePerSm) : solve_smem_bytes(a.arena_bytes);
-  return launch_pdl(k_solve, dim3((unsigned)B), dim3(T), smem, st, a);
+  SolveArgs a = a0;
+  if (cpsm == 1 && a.arena_bytes == 0) a.arena_bytes = kBigArena;
+  return launch_pdl(k_solve, dim3((unsigned)B), dim3(T), solve_smem_bytes(a.arena_bytes), st, a);
 }
 
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st) {

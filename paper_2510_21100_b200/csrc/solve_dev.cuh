@@ -70,9 +70,17 @@ constexpr int kProfBlock = 0;
       g_solve_nclk = prof_n;                                                         \
     }                                                                                \
   } while (0)
+// fixed-slot marks (run_build steps, Eq. 20 steps): g_solve_clk[600 + slot]
+#define SLOT_MARK(slot)                                                                \
+  do {                                                                                 \
+    if (blockIdx.x == kProfBlock && threadIdx.x == 0) g_solve_clk[600 + (slot)] = clock64(); \
+  } while (0)
 #else
 #define PROF_MARK() \
   do {              \
+  } while (0)
+#define SLOT_MARK(slot) \
+  do {                  \
   } while (0)
 #endif
 
@@ -284,8 +292,10 @@ struct RunArena {
 // scan of the per-slot piece counts places every piece in bin order.  Placement: after the
 // keys in shared memory when it fits (mask tail excluded), else arenaG.
 __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* mask, unsigned char* arenaS,
-                          int arenaBytes, bool keysInSmem, unsigned char* arenaG, RunArena& A, int* wscr) {
+                          int arenaBytes, bool keysInSmem, unsigned char* arenaG, RunArena& A, int* wscr,
+                          int pslot = 0) {
   const int tid = threadIdx.x;
+  SLOT_MARK(pslot + 0);
   const int E = nR * nL;
   for (int i = tid; i < kLevels * 8; i += T) mask[i] = 0u;
   const int e0 = (int)((long long)E * tid / T), e1 = (int)((long long)E * (tid + 1) / T);
@@ -302,6 +312,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   }
   int RR;
   int r = block_scan_excl(cnt, &RR, wscr);
+  SLOT_MARK(pslot + 1);
   const int Pmax = RR + E / kPiece;
   HR_CHECK(RR >= nR && RR <= E && RR <= kMaxRuns);
   const int keysS = keysInSmem ? align16(E) : 0;
@@ -326,6 +337,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     }
   }
   __syncthreads();
+  SLOT_MARK(pslot + 2);
   // hi = next run's lo - 1 in the same row (else nL - 1); bin masks
   const int r0 = (int)((long long)RR * tid / T), r1 = (int)((long long)RR * (tid + 1) / T);
   for (int q = r0; q < r1; ++q) {
@@ -343,6 +355,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   int kcount = 0;
 #pragma unroll
   for (int u = 0; u < 8; ++u) kcount += __popc(mask[tid * 8 + u]);
+  SLOT_MARK(pslot + 3);
   int RK;
   const int kfirst = block_scan_excl(kcount, &RK, wscr);  // first run slot of bin tid
   s.keyStart[tid] = kfirst;
@@ -355,6 +368,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)] = (uint32_t)((hi - lo) / kPiece + 1);
   }
   __syncthreads();
+  SLOT_MARK(pslot + 4);
   int np = 0;  // exclusive scan of the bin-ordered piece counts -> piece offsets
   for (int q = r0; q < r1; ++q) np += (int)slotN[q];
   int P;
@@ -367,6 +381,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   A.P = P;
   HR_CHECK(P >= RR && P <= Pmax && RK == RR);
   __syncthreads();
+  SLOT_MARK(pslot + 5);
   for (int q = r0; q < r1; ++q) {  // pieces of each run at its bin-order offset
     const uint32_t d = runDesc[q];
     const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
@@ -379,6 +394,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   s.keyStart[tid] = kfirst < RK ? (int)slotN[kfirst] : P;  // run slots -> piece offsets
   if (tid == 0) s.keyStart[kLevels] = P;
   __syncthreads();
+  SLOT_MARK(pslot + 6);
 }
 
 // sum of h[lo..hi] (hi - lo < kPiece): all loads predicated and in flight at once, fixed tree
@@ -713,7 +729,8 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
     kc1[e] = __ldg(args.idx1_tab + s.listR[a] * kLevels + s.listL[c]);
   }
   __syncthreads();
-  run_build(s, nR, nL, kc1, mask, arenaS, AB, keysS, arenaG, A, wscr);
+  SLOT_MARK(20);
+  run_build(s, nR, nL, kc1, mask, arenaS, AB, keysS, arenaG, A, wscr, 10);
   for (int p = tid; p < A.P; p += T) {  // piece values hR_a * sum(hL over the piece)
     const uint32_t d = A.pDesc[p];
     const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;

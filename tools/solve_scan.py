@@ -49,7 +49,11 @@ for cfg, nimg in (("C3", 64), ("C5", 64), ("C2", 1), ("C4", 1)):
         full = (ctypes.c_longlong * 1024)()
         lib.hr_debug_solve_clocks_all(full)
         nL, nR = int((hs[b] > 0).sum()), int((hg[b] > 0).sum())
-        rows.append((int(c[-1] - c[0]), b, nL, nR, d.tolist(), [int(v) for v in full[512:516]], int(it.item())))
+        sl = [int(v) for v in full[600:621]]
+        rb1 = [sl[i + 1] - sl[i] for i in range(6)]
+        rb2 = [sl[11 + i] - sl[10 + i] for i in range(6)]
+        rows.append((int(c[-1] - c[0]), b, nL, nR, d.tolist(), [int(v) for v in full[512:516]], int(it.item()),
+                     rb1, rb2))
     tot = np.array([r[0] for r in rows]) / GHZ / 1e3
     print(f"== {cfg}: {B} images, solve latency us: min {tot.min():.1f} p50 {np.median(tot):.1f} "
           f"p90 {np.percentile(tot, 90):.1f} max {tot.max():.1f}")
@@ -57,3 +61,5 @@ for cfg, nimg in (("C3", 64), ("C5", 64), ("C2", 1), ("C4", 1)):
         print(f"   img {r[1]:3d} nL={r[2]:3d} nR={r[3]:3d} E={r[2] * r[3]:5d} iters={r[6]:2d} "
               f"total {r[0] / GHZ / 1e3:6.1f} us  [hist,supp,runs,iters,eq20]={r[4]}  per-iter [E1,E2,R,L]="
               f"{[round(v / max(r[6], 1)) for v in r[5]]}")
+        print(f"      run_build steps [count+scan, desc, fix+mask, keyscan, slots, pieces+scan/write]: {r[7]}"
+              f"  eq20 build: {r[8]}")
