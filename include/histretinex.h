@@ -223,6 +223,8 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
      "hist_cpsm", "apply_cpsm"  unfused kernels' CTAs per SM (1..2)         default 2
      "warp_solver"  unfused path: warp-per-image solver for small supports   default 0
      "solve_cpsm"   solver CTAs per SM: 1, 2, 0 = auto (1 when B <= #SMs)   default 0
+     "apply_dyn"    separate kernels: the apply takes images in the order their  default 0
+                    LUTs complete (completion queue filled by the solver)
      "hist_overlap" separate kernels: each solver CTA starts when its image's  default 0
                     histogram segments are flushed (histograms at 2x256 threads per SM)
    The environment variables HR_<KEY upper-cased> set the initial values at hr_create.

@@ -123,6 +123,8 @@ struct SolveArgs {
   const uint8_t* idx1_tab;  // [256][256] index_1(i, j) for params.gamma (launch_idx1_table)
   const int32_t* only_deferred;  // k_solve: when set, images with only_deferred[b] == 0 are skipped
   uint32_t* ready;               // [B] nullable (k_solve): released (= 1) once image b's LUT is written
+  uint32_t* queue;               // [B] nullable (k_solve): completion queue, queue[i] = (i-th finished b) + 1
+  uint32_t* queue_tail;          // ... its tail counter
   const uint32_t* hist_done;     // [B] nullable (k_solve): start image b once all its segments flushed
   int32_t hist_grid;             // ... k_hist's grid (the segment count follows from it)
   int32_t hist_H;                // ... rows per image
@@ -144,6 +146,11 @@ cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B
 // does not wait for the solver grid to finish but acquires ready[b] before image b's table
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
                          uint8_t* out, int grid_ctas, cudaStream_t st, const uint32_t* ready = nullptr);
+// dynamic apply: warps take groups of GS chunks of the images in LUT-completion order (queue
+// filled by k_solve); false when the shape needs the scalar path (then use launch_apply)
+bool apply_dyn_supported(const uint8_t* in, const uint8_t* out, int64_t B, int32_t H, int32_t W);
+cudaError_t launch_apply_dyn(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
+                             int grid_ctas, const uint32_t* queue, uint32_t* ticket, int GS, cudaStream_t st);
 // second workload (k_quality.cu): HE LUT per image (Eq. 4-5) and the quality metrics
 cudaError_t launch_he_lut(const uint32_t* hist_s, int64_t B, uint8_t* lut, cudaStream_t st);
 size_t quality_ws_bytes(int64_t B, int32_t H, int32_t W);
@@ -154,7 +161,9 @@ cudaError_t launch_zero(void* p, size_t n, cudaStream_t st);
 
 // Persistent fused kernel (k_fused.cu): histograms -> per-image solve + LUT -> apply.
 constexpr int kCtlHeader = 32;  // control words before done[B]
-inline size_t fused_ctl_bytes(int64_t B) { return (size_t)(kCtlHeader + 2 * B) * sizeof(uint32_t); }
+// control block: [header | done[B] | ready[B] | queue[B]]; header word 2 = completion-queue
+// tail, word 3 = dynamic-apply ticket
+inline size_t fused_ctl_bytes(int64_t B) { return (size_t)(kCtlHeader + 3 * B) * sizeof(uint32_t); }
 struct FusedArgs {
   const uint8_t* in;  // [B][H][W][3]
   uint8_t* out;       // [B][H][W][3]

@@ -124,6 +124,120 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   if (lane == 0) bulk_wait<0>();
 }
 
+// ---------------------------------------------------------------- dynamic (completion-order) apply
+// The same per-warp TMA pipeline, fed by tickets over (completion-queue position, group of GS
+// chunks): the loader lane acquires queue[pos] (k_solve released it after writing that image's
+// LUT), so warps always work on images whose LUT is done and the apply starts with the first
+// finished solve.  Each new image's LUT is loaded into registers when its first chunk is issued
+// (kAhead chunks before it is computed).  Deadlock-free: launched (PDL) only once every solver
+// CTA is resident, and each solve fills one queue slot.
+__global__ void __launch_bounds__(kApplyThreads, 2)
+k_apply_dyn(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int64_t B, int64_t HW,
+            uint8_t* __restrict__ out, const uint32_t* __restrict__ queue, uint32_t* __restrict__ ticket, uint32_t GS) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
+  __shared__ uint2 meta[kWarps][kStages];  // (image, chunk) of each stage, image = kEndImg: end
+  constexpr uint32_t kEndImg = 0xFFFFFFFFu;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  pdl_trigger();  // no grid-wide wait: LUTs arrive through the completion queue
+  if (lane == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(&s.bar[w][k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t cpi = (uint32_t)((HW + kChunkPx - 1) / kChunkPx);
+  const uint32_t gpi = (cpi + GS - 1) / GS;
+  const uint64_t ngroups = (uint64_t)B * gpi;
+  const uint64_t pol = policy_evict_first();
+  uint2* tab = s.tab[w];
+  // loader state (lane 0): image and chunk range of the current group, prefetched next ticket
+  uint32_t lb = 0, lc = 0, le = 0, nxt = 0;
+  if (lane == 0) nxt = atomicAdd(ticket, 1u);
+  auto next_chunk = [&](uint32_t& b, uint32_t& c) -> bool {
+    if (lc >= le) {
+      if (nxt >= ngroups) return false;
+      const uint32_t q = nxt / gpi, g = nxt - q * gpi;
+      uint32_t v;
+      while ((v = ld_acquire(queue + q)) == 0u) __nanosleep(100);
+      lb = v - 1u;
+      lc = g * GS;
+      le = min(lc + GS, cpi);
+      nxt = atomicAdd(ticket, 1u);
+    }
+    b = lb;
+    c = lc++;
+    return true;
+  };
+  uint32_t ld_img = kEndImg, pend_img = kEndImg;
+  uint2 pend = make_uint2(0u, 0u);
+  auto issue = [&](uint32_t i) {  // all lanes; lane 0 fills stage i % kStages
+    const int st = (int)(i % kStages);
+    uint32_t b = kEndImg, c = 0;
+    if (lane == 0 && !next_chunk(b, c)) b = kEndImg;
+    b = __shfl_sync(0xffffffffu, b, 0);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    __syncwarp();  // lane 0's queue acquire before the other lanes read this image's LUT
+    if (lane == 0) meta[w][st] = make_uint2(b, c);
+    if (b == kEndImg) {
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s.bar[w][st])) : "memory");
+      return;
+    }
+    if (b != ld_img) {
+      ld_img = b;
+      if (pend_img == kEndImg) {
+        pend = __ldcg(reinterpret_cast<const uint2*>(lut + (uint64_t)b * kLevels) + lane);
+        pend_img = b;
+      }
+    }
+    if (lane == 0) {
+      const uint32_t px0 = c * kChunkPx, npx = min((uint32_t)kChunkPx, (uint32_t)(HW - px0));
+      const uint64_t off = ((uint64_t)b * (uint64_t)HW + px0) * 3u;
+      mbar_expect_tx(&s.bar[w][st], npx * 3u);
+      bulk_load(s.stage[w][st], in + off, npx * 3u, &s.bar[w][st], pol);
+    }
+  };
+  for (uint32_t i = 0; i < (uint32_t)kAhead; ++i) issue(i);
+  uint32_t cur_img = kEndImg;
+  int st = 0;
+  uint32_t ph = 0;
+  for (uint32_t i = 0;; ++i) {
+    if (lane == 0 && i >= 2) bulk_wait_read<1>();
+    __syncwarp();
+    issue(i + kAhead);
+    mbar_wait(&s.bar[w][st], ph);
+    const uint2 m = meta[w][st];
+    if (m.x == kEndImg) break;  // warp-uniform
+    const uint32_t b = m.x, px0 = m.y * kChunkPx;
+    const uint32_t bytes = min((uint32_t)kChunkPx, (uint32_t)(HW - px0)) * 3u;
+    const uint64_t off = ((uint64_t)b * (uint64_t)HW + px0) * 3u;
+    HR_CHECK(b < B && bytes > 0 && bytes <= (uint32_t)kChunkBytes);
+    if (b != cur_img) {
+      __syncwarp();
+      if (b == pend_img) {
+        build_tab_regs(tab, pend, lane);
+        pend_img = kEndImg;
+      } else {
+        build_tab(tab, lut + (uint64_t)b * kLevels, lane);  // queue order implies the LUT is done
+      }
+      __syncwarp();
+      cur_img = b;
+    }
+    uint8_t* p = s.stage[w][st];
+    apply_chunk_smem(p, bytes, tab, lane);
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      bulk_store(out + off, p, bytes, pol);
+      bulk_commit();
+    }
+    if (++st == kStages) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+  if (lane == 0) bulk_wait<0>();
+}
+
 // ---------------------------------------------------------------- scalar fallback
 __device__ __forceinline__ void apply_scalar(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int64_t q,
                                              const uint32_t* ab) {
@@ -154,6 +268,25 @@ k_apply_scalar(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, 
 }
 
 }  // namespace
+
+bool apply_dyn_supported(const uint8_t* in, const uint8_t* out, int64_t B, int32_t H, int32_t W) {
+  const int64_t HW = (int64_t)H * W;
+  return reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 && HW % 16 == 0 &&
+         B * ((HW + kChunkPx - 1) / kChunkPx) < (1LL << 31);
+}
+
+cudaError_t launch_apply_dyn(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
+                             int grid_ctas, const uint32_t* queue, uint32_t* ticket, int GS, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_apply_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ApplySmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t HW = (int64_t)H * W;
+  return launch_pdl(k_apply_dyn, dim3((unsigned)(grid_ctas < 1 ? 1 : grid_ctas)), dim3(kApplyThreads),
+                    sizeof(ApplySmem), st, in, lut, B, HW, out, queue, ticket, (uint32_t)(GS < 1 ? 1 : GS));
+}
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
                          int grid_ctas, cudaStream_t st, const uint32_t* ready) {

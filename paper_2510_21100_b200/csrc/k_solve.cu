@@ -30,10 +30,13 @@ __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
     pdl_trigger();
   }
   solve_image(args, blockIdx.x, smraw, wscr);
-  if (args.ready) {  // every exit of solve_image arrives here: LUT written -> release ready[b]
+  if (args.ready || args.queue) {  // every exit of solve_image arrives here: LUT written
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) st_release(args.ready + blockIdx.x, 1u);
+    if (threadIdx.x == 0) {
+      if (args.ready) st_release(args.ready + blockIdx.x, 1u);
+      if (args.queue) st_release(args.queue + atomicAdd(args.queue_tail, 1u), (uint32_t)blockIdx.x + 1u);
+    }
   }
 }
 
