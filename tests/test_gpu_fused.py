@@ -148,3 +148,21 @@ def test_enhance_host_rejects_bad_args():
     m = hr()
     with pytest.raises(ValueError):
         m.hr_enhance_host(torch.zeros((2, 4, 4, 3), dtype=torch.uint8, device="cuda"))
+
+
+@pytest.mark.parametrize("knob", ["apply_dyn", "hist_overlap"])
+@pytest.mark.parametrize("shape", [(2, 4, 4), (3, 37, 112), (4, 30, 24), (40, 16, 32), (300, 8, 16), (2, 37, 101)])
+def test_policy_options_bit_exact(knob, shape):
+    """The optional separate-kernel schedules (completion-order apply from the solver's queue;
+    solvers starting per image during the histogram pass) change only the schedule."""
+    m = hr()
+    x = torch.from_numpy(batch(*shape, seed0=17)).cuda()
+    ref = [t.cpu() for t in m.hr_enhance_debug(x)]
+    m.set_policy(knob, 1)
+    try:
+        got = [t.cpu() for t in m.hr_enhance_debug(x)]
+        got2 = [t.cpu() for t in m.hr_enhance_debug(x)]  # back-to-back: the queue state resets
+    finally:
+        m.set_policy(knob, 0)
+    for a, b, c in zip(ref, got, got2):
+        assert torch.equal(a, b) and torch.equal(a, c)
