@@ -506,10 +506,24 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         s.hL2[tid] = n * n;
         q = n * n;
       }
-      for (int p = tid; p < A.P; p += T) {  // piece sums hR_a * sum(hL over the piece)
-        const uint32_t d = A.pDesc[p];
-        const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;
-        A.pVal[p] = s.hR1[pa] * piece_sum(s.hL1, lo, hi) * cRL;
+      {  // piece sums hR_a * sum(hL over the piece); two pieces per step so that their loads
+         // are in flight together (restrict: the stores to pVal cannot alias the loads)
+        const uint32_t* __restrict__ pd = A.pDesc;
+        double* __restrict__ pv = A.pVal;
+        const double* __restrict__ hl1 = s.hL1;
+        const double* __restrict__ hr1 = s.hR1;
+        int p = tid;
+        for (; p + T < A.P; p += 2 * T) {
+          const uint32_t d0 = pd[p], d1 = pd[p + T];
+          const double v0 = hr1[d0 >> 16] * piece_sum(hl1, d0 & 255, (d0 >> 8) & 255) * cRL;
+          const double v1 = hr1[d1 >> 16] * piece_sum(hl1, d1 & 255, (d1 >> 8) & 255) * cRL;
+          pv[p] = v0;
+          pv[p + T] = v1;
+        }
+        if (p < A.P) {
+          const uint32_t d = pd[p];
+          pv[p] = hr1[d >> 16] * piece_sum(hl1, d & 255, (d >> 8) & 255) * cRL;
+        }
       }
       if (t == 0 || P.use_epsilon) slot_put3(s, R_DR, dr, R_DL, dl, R_SL2, q);
     }
