@@ -223,10 +223,17 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
      "hist_cpsm", "apply_cpsm"  unfused kernels' CTAs per SM (1..2)         default 2
      "warp_solver"  unfused path: warp-per-image solver for small supports   default 0
      "solve_cpsm"   solver CTAs per SM: 1, 2, 0 = auto (1 when B <= #SMs)   default 0
-     "apply_dyn"    separate kernels: the apply takes images in the order their  default 0
-                    LUTs complete (completion queue filled by the solver)
+     "apply_dyn"    separate kernels: 1 = the apply takes images in the order     default 0
+                    their LUTs complete (completion queue filled by the solver);
+                    2 = natural order after the solver grid; both with per-warp
+                    tickets of apply_gs chunks that balance the streaming work
+     "apply_gs"     1024-pixel chunks per dynamic-apply warp ticket (>= 1)      default 8
      "hist_overlap" separate kernels: each solver CTA starts when its image's  default 0
                     histogram segments are flushed (histograms at 2x256 threads per SM)
+     "hist_tma"     histogram kernel with TMA-staged rows (one CTA per SM; in     default 0
+                    the hist_overlap form 512 threads in image waves) for 16-B
+                    aligned batches with W % 16 == 0 (256 <= W <= 8192) or
+                    W % 16 == 8 (128 <= W <= 4096, B*H*W*3 % 16 == 0)
    The environment variables HR_<KEY upper-cased> set the initial values at hr_create.
    Returns HR_EINVAL for an unknown key or an out-of-range value (nothing changes). */
 hr_status hr_set_policy(hr_ctx* ctx, const char* key, int64_t value);

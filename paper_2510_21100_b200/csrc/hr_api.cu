@@ -33,8 +33,11 @@ struct hr_ctx {
   int fused_bands = 2;    // histogram band items per CTA (sets bands per image)
   int fused_gs = 8;       // 1024-px chunks per apply ticket
   int solve_cpsm = 0;     // k_solve CTAs per SM: 1, 2, or 0 = auto (1 when B <= SMs)
-  int apply_dyn = 0;      // separate kernels: the apply takes images in LUT-completion order
+  int apply_gs = 8;       // dynamic apply: 1024-px chunks per warp ticket
+  int apply_dyn = 0;      // separate kernels: 1 = the apply takes images in LUT-completion order,
+                          // 2 = natural order after the solver grid, warp tickets balancing the work
                           // (off: per-warp tickets scatter the streams; C3 0.364 vs 0.269 ms)
+  int hist_tma = 0;       // k_hist: TMA-staged rows where the shape allows (off: measured no faster)
   int hist_overlap = 0;   // separate kernels: solves start per image beside a 2x256-thread histogram pass
                           // (off: the 16-warp histogram pass costs more than the overlap saves)
   int64_t launches = 0;   // kernels launched through this context (hr_kernel_launches)
@@ -203,7 +206,9 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_FUSED_GS")) c->fused_gs = atoi(v) > 0 ? atoi(v) : 8;
   if (const char* v = getenv("HR_SOLVE_CPSM")) c->solve_cpsm = atoi(v) >= 0 && atoi(v) <= 2 ? atoi(v) : 0;
   if (const char* v = getenv("HR_HIST_OVERLAP")) c->hist_overlap = atoi(v) != 0;
-  if (const char* v = getenv("HR_APPLY_DYN")) c->apply_dyn = atoi(v) != 0;
+  if (const char* v = getenv("HR_HIST_TMA")) c->hist_tma = atoi(v) != 0;
+  if (const char* v = getenv("HR_APPLY_DYN")) c->apply_dyn = atoi(v) >= 0 && atoi(v) <= 2 ? atoi(v) : 0;
+  if (const char* v = getenv("HR_APPLY_GS")) c->apply_gs = atoi(v) > 0 ? atoi(v) : 8;
   *out = c;
   return HR_OK;
 }
@@ -250,7 +255,7 @@ hr_status hr_set_policy(hr_ctx* c, const char* key, int64_t v) {
       {"chunks", &c->chunks, 1, 1 << 16},           {"hist_cpsm", &c->hist_cpsm, 1, 2},
       {"apply_cpsm", &c->apply_cpsm, 1, 2},         {"warp_solver", &c->warp_solver, 0, 1},
       {"solve_cpsm", &c->solve_cpsm, 0, 2},         {"hist_overlap", &c->hist_overlap, 0, 1},
-      {"apply_dyn", &c->apply_dyn, 0, 1},
+      {"apply_dyn", &c->apply_dyn, 0, 2},           {"apply_gs", &c->apply_gs, 1, 1 << 20},           {"hist_tma", &c->hist_tma, 0, 1},
   };
   for (const Knob& k : knobs) {
     if (strcmp(k.name, key) != 0) continue;
@@ -319,7 +324,7 @@ hr_status hr_histogram(hr_ctx* c, const uint8_t* rgb, int64_t B, int32_t H, int3
   uint32_t* graw = hist_g_raw ? hist_g_raw : reinterpret_cast<uint32_t*>((char*)ws + L.graw);
   cudaError_t e = cudaMemsetAsync(hist_s, 0, (size_t)B * kLevels * sizeof(uint32_t), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(graw, 0, (size_t)B * kGradSlots * sizeof(uint32_t), st);
-  if (e == cudaSuccess) e = counted(c, hr::launch_hist(rgb, B, H, W, hist_s, graw, hist_grid(c), st));
+  if (e == cudaSuccess) e = counted(c, hr::launch_hist(rgb, B, H, W, hist_s, graw, hist_grid(c), st, hr::kHistThreads, nullptr, c->hist_tma));
   if (e == cudaSuccess) e = counted(c, hr::launch_remap(graw, B, grad_norm, hist_g, st));
   return cuda_err(c, e, "hr_histogram");
 }
@@ -434,7 +439,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   auto hist_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s) -> cudaError_t {
     cudaError_t r = counted(c, hr::launch_zero(hs + b0 * kLevels, (size_t)nb * kLevels * sizeof(uint32_t), s));
     if (r == cudaSuccess) r = counted(c, hr::launch_zero(graw + b0 * kGradSlots, (size_t)nb * kGradSlots * sizeof(uint32_t), s));
-    if (r == cudaSuccess) r = counted(c, hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, hist_grid(c), s));
+    if (r == cudaSuccess) r = counted(c, hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, hist_grid(c), s, hr::kHistThreads, nullptr, c->hist_tma));
     return r;
   };
   auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, uint32_t* ready = nullptr,
@@ -445,7 +450,6 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     a.queue = c->warp_solver ? nullptr : queue;
     a.queue_tail = queue_tail;
     a.hist_done = c->warp_solver ? nullptr : hist_done;
-    a.hist_grid = hist_bands;  // the histogram kernel's (clamped) grid
     a.hist_H = H;
     a.arena_bytes = hist_done ? kOverlapArena : 0;  // fits beside two histogram CTAs
     a.idx1_tab = tab;
@@ -538,24 +542,25 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       if (e == cudaSuccess)
         e = counted(c, hr::launch_zero((char*)ws + z0, align_up(L.ctl + hr::fused_ctl_bytes(B)) - z0, st));
     }
-    // histograms at 2 x 256 threads per SM counting flushed segments per image: each solver CTA
-    // (beside them) starts once its image is complete (needs the zeroed control block)
+    // histograms counting flushed rows per image (TMA-staged kernel in image waves, 512 threads
+    // per SM; else the direct-load kernel at 2 x 256 threads per SM): each solver CTA, resident
+    // beside them, starts once its image is complete (needs the zeroed control block)
     const bool overlap = c->hist_overlap && ready && !c->warp_solver;
     uint32_t* ctl = reinterpret_cast<uint32_t*>((char*)ws + L.ctl);
     const int HG = hr::hist_grid_clamped(B, H, 2 * c->num_sms);
     if (e == cudaSuccess)
-      e = overlap ? counted(c, hr::launch_hist(in, B, H, W, hs, graw, HG, st, 256, ctl + hr::kCtlHeader))
-                  : counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st));
+      e = overlap ? counted(c, hr::launch_hist(in, B, H, W, hs, graw, HG, st, 256, ctl + hr::kCtlHeader, c->hist_tma))
+                  : counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st, hr::kHistThreads, nullptr, c->hist_tma));
     if (e == cudaSuccess) e = mark(1);
     // completion-order apply: k_solve appends each finished image to a queue in the control block
     const bool dyn = c->apply_dyn && ready && !c->warp_solver && hr::apply_dyn_supported(in, out, B, H, W);
-    uint32_t* queue = dyn ? ctl + hr::kCtlHeader + 2 * B : nullptr;
+    uint32_t* queue = dyn && c->apply_dyn == 1 ? ctl + hr::kCtlHeader + 2 * B : nullptr;
     if (e == cudaSuccess)
       e = solve_chunk(0, B, st, ready, overlap ? ctl + hr::kCtlHeader : nullptr, overlap ? HG : 0, queue,
-                      dyn ? ctl + 2 : nullptr);
+                      queue ? ctl + 2 : nullptr);
     if (e == cudaSuccess) e = mark(2);
     if (e == cudaSuccess)
-      e = dyn ? counted(c, hr::launch_apply_dyn(in, lut, B, H, W, out, apply_grid(c), queue, ctl + 3, 8, st))
+      e = dyn ? counted(c, hr::launch_apply_dyn(in, lut, B, H, W, out, apply_grid(c), queue, ctl + 3, c->apply_gs, st))
               : apply_chunk(0, B, st, ready);
     if (e == cudaSuccess) e = mark(3);
     return cuda_err(c, e, "hr_enhance");
@@ -618,7 +623,7 @@ hr_status hr_he(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, u
   uint8_t* lut = lut_dbg ? lut_dbg : reinterpret_cast<uint8_t*>((char*)ws + L.lut);
   cudaError_t e = counted(c, hr::launch_zero(hs, (size_t)B * kLevels * sizeof(uint32_t), st));
   if (e == cudaSuccess) e = counted(c, hr::launch_zero(graw, (size_t)B * kGradSlots * sizeof(uint32_t), st));
-  if (e == cudaSuccess) e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st));
+  if (e == cudaSuccess) e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st, hr::kHistThreads, nullptr, c->hist_tma));
   if (e == cudaSuccess) e = counted(c, hr::launch_he_lut(hs, B, lut, st));
   if (e == cudaSuccess) e = counted(c, hr::launch_apply(in, lut, B, H, W, out, apply_grid(c), st));
   return cuda_err(c, e, "hr_he");
@@ -689,3 +694,13 @@ hr_status hr_enhance_host(hr_ctx* c, const uint8_t* in_h, int64_t B, int32_t H, 
 }
 
 }  // extern "C"
+
+#ifdef HR_STEP_TRACE
+// measurement-only (tools/step_trace.py; not part of histretinex.h): bind the step-timeline buffer
+extern "C" int hr_debug_trace_bind(void* buf, uint32_t* n, uint32_t cap) {
+  hr::trace_bind_hist(buf, n, cap);
+  hr::trace_bind_solve(buf, n, cap);
+  hr::trace_bind_apply(buf, n, cap);
+  return (int)cudaGetLastError();
+}
+#endif

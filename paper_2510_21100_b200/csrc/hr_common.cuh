@@ -31,6 +31,60 @@ namespace hr {
   } while (0)
 #endif
 
+// ---- step timeline (measurement builds only: -DHR_STEP_TRACE; tools/step_trace.py) ----
+// Thread 0 of every CTA of k_hist / k_solve / k_apply appends {kernel, CTA, SM, aux, start, end}
+// (globaltimer ns) to a host-bound buffer; aux = the image a solver CTA solved (its wait for the
+// image's histogram ends at `mid`).  Each translation unit holds its own pointer copies, bound
+// by hr_debug_trace_bind.
+#ifdef HR_STEP_TRACE
+struct TraceRec {
+  uint32_t kind, cta, sm, aux;
+  unsigned long long t0, mid, t1, pad;
+};
+namespace {
+__device__ TraceRec* g_trace = nullptr;
+__device__ uint32_t* g_trace_n = nullptr;
+__device__ uint32_t g_trace_cap = 0;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+__device__ __forceinline__ void trace_rec(uint32_t kind, uint32_t aux, unsigned long long t0, unsigned long long mid) {
+  if (threadIdx.x == 0 && g_trace) {
+    const uint32_t i = atomicAdd(g_trace_n, 1u);
+    if (i < g_trace_cap) g_trace[i] = TraceRec{kind, blockIdx.x, smid(), aux, t0, mid, gtime(), 0ull};
+  }
+}
+inline void trace_bind_tu(void* buf, uint32_t* n, uint32_t cap) {
+  cudaMemcpyToSymbol(g_trace, &buf, sizeof(void*));
+  cudaMemcpyToSymbol(g_trace_n, &n, sizeof(void*));
+  cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof(uint32_t));
+}
+}  // namespace
+#define TRACE_T0() const unsigned long long tr_t0_ = gtime()
+#define TRACE_MID(v) v = gtime()
+#define TRACE_END(kind, aux, mid) trace_rec((kind), (aux), tr_t0_, (mid))
+#else
+#define TRACE_T0() \
+  do {             \
+  } while (0)
+#define TRACE_MID(v) \
+  do {               \
+  } while (0)
+#define TRACE_END(kind, aux, mid) \
+  do {                            \
+  } while (0)
+#endif
+void trace_bind_hist(void* buf, uint32_t* n, uint32_t cap);
+void trace_bind_solve(void* buf, uint32_t* n, uint32_t cap);
+void trace_bind_apply(void* buf, uint32_t* n, uint32_t cap);
+
 // ---- programmatic dependent launch (PDL) ----
 // Kernels of a step are launched with programmatic stream serialization: a kernel's launch
 // (CTA rasterisation, shared-memory carve-out) overlaps its predecessor's tail.  Every such
@@ -91,17 +145,23 @@ constexpr int kApplyThreads = 256;
 
 // Launch helpers implemented in the kernel translation units.
 // nt: threads per CTA (512, or 256 to leave room for a solver CTA); done (nullable): per-image
-// counts of flushed segments (see hist_segments_of)
+// counts of flushed rows (a segment of image b adds its row count to done[b] after its flush);
+// tma: use the TMA-staged kernel when the shape allows it (tma_hist_supported): one CTA per SM
+// (grid / 2), and with done: 512 threads at <= 64 registers in image waves
+// (hist_wave_images), leaving registers and shared memory for one solver CTA per SM
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
                         uint32_t* hist_graw, int grid, cudaStream_t st, int nt = kHistThreads,
-                        uint32_t* done = nullptr);
+                        uint32_t* done = nullptr, int tma = 1);
 int hist_grid_clamped(int64_t B, int32_t H, int grid);  // the grid launch_hist actually uses
-// number of k_hist CTA row ranges [R c / G, R (c+1) / G) overlapping image b's rows [bH, (b+1)H)
-__host__ __device__ inline int hist_segments_of(int64_t b, int64_t H, int64_t R, int64_t G) {
-  const int64_t first = ((b * H + 1) * G + R - 1) / R - 1;      // min c with R (c+1) / G > bH
-  int64_t last = ((b + 1) * H * G + R - 1) / R - 1;             // max c with R c / G < (b+1) H
-  if (last > G - 1) last = G - 1;
-  return (int)(last - first + 1);
+bool tma_hist_supported(const uint8_t* rgb, int64_t B, int32_t H, int32_t W);
+// Wave order of the TMA histogram kernel with per-image completion counts: images
+// [w k, min(B, (w + 1) k)) form wave w and CTA c of G takes rows [R_w c / G, R_w (c + 1) / G) of
+// the wave (R_w = its images x H), so the images of wave w are complete once every CTA has
+// passed wave w.  Returns the images per wave for a target of ~rows_per_cta rows per CTA.
+__host__ __device__ inline int64_t hist_wave_images(int64_t B, int64_t H, int64_t G, int64_t rows_per_cta) {
+  int64_t k = (rows_per_cta * G + H - 1) / H;
+  if (k < 1) k = 1;
+  return k < B ? k : B;
 }
 cudaError_t launch_remap(const uint32_t* hist_graw, int64_t B, int32_t grad_norm, uint32_t* hist_g,
                          cudaStream_t st);
@@ -125,9 +185,8 @@ struct SolveArgs {
   uint32_t* ready;               // [B] nullable (k_solve): released (= 1) once image b's LUT is written
   uint32_t* queue;               // [B] nullable (k_solve): completion queue, queue[i] = (i-th finished b) + 1
   uint32_t* queue_tail;          // ... its tail counter
-  const uint32_t* hist_done;     // [B] nullable (k_solve): start image b once all its segments flushed
-  int32_t hist_grid;             // ... k_hist's grid (the segment count follows from it)
-  int32_t hist_H;                // ... rows per image
+  const uint32_t* hist_done;     // [B] nullable (k_solve): start image b once all its rows are flushed
+  int32_t hist_H;                // ... rows per image: image b is complete when hist_done[b] == hist_H
   int32_t arena_bytes;           // shared run arena per CTA (0: the default 80 KB)
   double* trace;                 // [B][trace_stride] nullable: Eq. 10 objective, 3 values per update
   int32_t trace_stride;

@@ -31,6 +31,7 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   extern __shared__ __align__(128) unsigned char smraw[];
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  TRACE_T0();
   if (!ready) pdl_wait();  // with per-image flags only the LUTs depend on the solver grid
   pdl_trigger();
   if (lane == 0) {
@@ -122,13 +123,17 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
     }
   }
   if (lane == 0) bulk_wait<0>();
+  TRACE_END(4u, 0u, 0ull);
 }
 
-// ---------------------------------------------------------------- dynamic (completion-order) apply
-// The same per-warp TMA pipeline, fed by tickets over (completion-queue position, group of GS
-// chunks): the loader lane acquires queue[pos] (k_solve released it after writing that image's
-// LUT), so warps always work on images whose LUT is done and the apply starts with the first
-// finished solve.  Each new image's LUT is loaded into registers when its first chunk is issued
+// ---------------------------------------------------------------- dynamic (ticketed) apply
+// The same per-warp TMA pipeline, fed by tickets over (image position, group of GS chunks),
+// each warp's next ticket fetched while it works on the current one.  With a completion queue
+// the loader lane acquires queue[pos] (k_solve released it after writing that image's LUT), so
+// warps always work on images whose LUT is done and the apply starts with the first finished
+// solve; without one (queue == NULL) images go in natural order after the whole solver grid
+// (griddepcontrol.wait) -- the tickets then only balance the streaming work across warps
+// whatever their start times (CTAs that become resident late take fewer tickets).  Each new image's LUT is loaded into registers when its first chunk is issued
 // (kAhead chunks before it is computed).  Deadlock-free: launched (PDL) only once every solver
 // CTA is resident, and each solve fills one queue slot.
 __global__ void __launch_bounds__(kApplyThreads, 2)
@@ -139,7 +144,11 @@ k_apply_dyn(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   __shared__ uint2 meta[kWarps][kStages];  // (image, chunk) of each stage, image = kEndImg: end
   constexpr uint32_t kEndImg = 0xFFFFFFFFu;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  pdl_trigger();  // no grid-wide wait: LUTs arrive through the completion queue
+  TRACE_T0();
+  // with the completion queue there is no grid-wide wait: LUTs arrive through the queue;
+  // without it (natural image order) every LUT is read after the solver grid has completed
+  if (!queue) pdl_wait();
+  pdl_trigger();
   if (lane == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&s.bar[w][k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -157,9 +166,13 @@ k_apply_dyn(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
     if (lc >= le) {
       if (nxt >= ngroups) return false;
       const uint32_t q = nxt / gpi, g = nxt - q * gpi;
-      uint32_t v;
-      while ((v = ld_acquire(queue + q)) == 0u) __nanosleep(100);
-      lb = v - 1u;
+      if (queue) {
+        uint32_t v;
+        while ((v = ld_acquire(queue + q)) == 0u) __nanosleep(100);
+        lb = v - 1u;
+      } else {
+        lb = q;
+      }
       lc = g * GS;
       le = min(lc + GS, cpi);
       nxt = atomicAdd(ticket, 1u);
@@ -236,6 +249,7 @@ k_apply_dyn(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
     }
   }
   if (lane == 0) bulk_wait<0>();
+  TRACE_END(5u, 0u, 0ull);
 }
 
 // ---------------------------------------------------------------- scalar fallback
@@ -269,6 +283,14 @@ k_apply_scalar(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, 
 
 }  // namespace
 
+void trace_bind_apply(void* buf, uint32_t* n, uint32_t cap) {
+#ifdef HR_STEP_TRACE
+  trace_bind_tu(buf, n, cap);
+#else
+  (void)buf, (void)n, (void)cap;
+#endif
+}
+
 bool apply_dyn_supported(const uint8_t* in, const uint8_t* out, int64_t B, int32_t H, int32_t W) {
   const int64_t HW = (int64_t)H * W;
   return reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 && HW % 16 == 0 &&
@@ -298,6 +320,9 @@ cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(k_apply_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)sizeof(ApplySmem));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_apply_tma, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxShared);
       if (e != cudaSuccess) return e;
       attr = true;
     }

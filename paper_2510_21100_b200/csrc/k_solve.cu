@@ -13,11 +13,13 @@ namespace {
 __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int wscr[NW];
-  if (args.hist_done) {  // overlap the histogram pass: wait for this image's segments only
+  TRACE_T0();
+  unsigned long long tr_mid = 0ull;
+  (void)tr_mid;
+  if (args.hist_done) {  // overlap the histogram pass: wait for this image's rows only
     pdl_trigger();
     if (threadIdx.x == 0) {
-      const int64_t Bn = gridDim.x, H = args.hist_H;
-      const uint32_t need = (uint32_t)hist_segments_of(blockIdx.x, H, Bn * H, args.hist_grid);
+      const uint32_t need = (uint32_t)args.hist_H;
       long long spins = 0;
       while (ld_acquire(args.hist_done + blockIdx.x) < need) {
         __nanosleep(256);
@@ -29,6 +31,7 @@ __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
     pdl_wait();
     pdl_trigger();
   }
+  TRACE_MID(tr_mid);
   solve_image(args, blockIdx.x, smraw, wscr);
   if (args.ready || args.queue) {  // every exit of solve_image arrives here: LUT written
     __threadfence();
@@ -38,6 +41,7 @@ __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
       if (args.queue) st_release(args.queue + atomicAdd(args.queue_tail, 1u), (uint32_t)blockIdx.x + 1u);
     }
   }
+  TRACE_END(3u, (uint32_t)blockIdx.x, tr_mid);
 }
 
 // index_1(i, j) of Eqs. 17-19 for every (i, j), once per gamma (R4, R5):
@@ -74,6 +78,14 @@ __global__ void __launch_bounds__(T) k_match(const uint32_t* hist_s, const doubl
 
 }  // namespace
 
+void trace_bind_solve(void* buf, uint32_t* n, uint32_t cap) {
+#ifdef HR_STEP_TRACE
+  trace_bind_tu(buf, n, cap);
+#else
+  (void)buf, (void)n, (void)cap;
+#endif
+}
+
 size_t solve_smem_bytes(int arena_bytes) { return sizeof(Sm) + (size_t)(arena_bytes > 0 ? arena_bytes : kArenaSmem); }
 size_t solve_cells_ws_bytes(int64_t B) { return (size_t)B * (size_t)kArenaGlobal; }
 
@@ -87,6 +99,8 @@ cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t 
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)solve_smem_bytes(kBigArena));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_solve, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     attr = true;
   }

@@ -150,15 +150,19 @@ def test_enhance_host_rejects_bad_args():
         m.hr_enhance_host(torch.zeros((2, 4, 4, 3), dtype=torch.uint8, device="cuda"))
 
 
-@pytest.mark.parametrize("knob", ["apply_dyn", "hist_overlap"])
-@pytest.mark.parametrize("shape", [(2, 4, 4), (3, 37, 112), (4, 30, 24), (40, 16, 32), (300, 8, 16), (2, 37, 101)])
+@pytest.mark.parametrize("knob", ["apply_dyn", "apply_dyn=2", "hist_overlap"])
+@pytest.mark.parametrize("shape", [(2, 4, 4), (3, 37, 112), (4, 30, 24), (40, 16, 32), (300, 8, 16), (2, 37, 101),
+                                   (2, 37, 264), (20, 45, 256), (5, 120, 600), (1, 300, 1920), (150, 16, 256)])
 def test_policy_options_bit_exact(knob, shape):
     """The optional separate-kernel schedules (completion-order apply from the solver's queue;
-    solvers starting per image during the histogram pass) change only the schedule."""
+    solvers starting per image during the histogram pass) change only the schedule.  The last
+    five shapes take the TMA histogram kernel in image waves under hist_overlap (W % 16 == 8 with
+    odd H; several waves; one image; more images than SMs)."""
     m = hr()
     x = torch.from_numpy(batch(*shape, seed0=17)).cuda()
     ref = [t.cpu() for t in m.hr_enhance_debug(x)]
-    m.set_policy(knob, 1)
+    knob, _, val = knob.partition("=")
+    m.set_policy(knob, int(val or 1))
     try:
         got = [t.cpu() for t in m.hr_enhance_debug(x)]
         got2 = [t.cpu() for t in m.hr_enhance_debug(x)]  # back-to-back: the queue state resets

@@ -6,3 +6,4 @@ F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -
 nvcc $F -DHR_SOLVE_PROFILE -o ../tools/libhistretinex_prof.so $SRC
 nvcc $F -DHR_FUSED_TRACE -o ../tools/libhistretinex_trace.so $SRC
 nvcc $F -DHR_CHECKS -o ../tools/libhistretinex_check.so $SRC
+nvcc $F -DHR_STEP_TRACE -o ../tools/libhistretinex_steptrace.so $SRC
