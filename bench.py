@@ -279,12 +279,14 @@ def run_ours(args, world, rank, local):
     hr.profile_enable(local, False)
     st0, st1, st2 = (v / max(nsteps, 1) for v in (st0, st1, st2))
     path = hr.last_path(local)  # 0 separate kernels, 1 fused, 2 chunk pipeline
-    fused, chunked = path == 1, path == 2
+    fused, chunked = path == 1, path in (2, 3)
     # informational: the separate-kernel stage split of the same workload (not the timed path)
     split = None
     if fused or chunked:
+        groups_used = hr.get_policy("groups", local)
         hr.set_policy("fused_min_b", 0, local)
         hr.set_policy("chunks", 1, local)
+        hr.set_policy("groups", 0, local)
         for _ in range(3):
             step()
         hr.profile_enable(local, True)
@@ -295,6 +297,7 @@ def run_ours(args, world, rank, local):
         hr.profile_enable(local, False)
         hr.set_policy("fused_min_b", int(os.environ.get("HR_FUSED_MIN_B", "0")), local)
         hr.set_policy("chunks", max(1, int(os.environ.get("HR_CHUNKS", "1"))), local)
+        hr.set_policy("groups", groups_used, local)
         split = (h_ms / max(n2, 1), s_ms / max(n2, 1), a_ms / max(n2, 1))
     else:
         split = (st0, st1, st2)
@@ -327,6 +330,16 @@ def run_ours(args, world, rank, local):
                "note": f"hr_enhance_host: pinned host in/out, H2D | enhance | D2H pipelined over "
                        f"{min(args.e2e_chunks or 8, B)} image chunks"}
 
+    if fused:
+        path_name = "fused persistent kernel (hist -> per-image solve + LUT -> apply)"
+    elif path == 3:
+        ng = groups_used if groups_used >= 2 else 2  # -1 = auto: 2 groups
+        path_name = (f"grouped step ({ng} image groups: hist(k+1) beside solve(k), apply beside the "
+                     "last group's solves)")
+    elif chunked:
+        path_name = "stream pipeline over image chunks"
+    else:
+        path_name = "separate kernels (hist | solve + LUT | apply)"
     value = aggregate_mps(world, B, H, W, ms)
     peak, peak_src = peaks()
     e2e_frac = BYTES_PER_PX * (B * H * W) / (ms / 1e3) / 1e9 / peak
@@ -372,9 +385,7 @@ def run_ours(args, world, rank, local):
             "roofline": {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": kbytes},
-            "path": "fused persistent kernel (hist -> per-image solve + LUT -> apply)" if fused
-                    else ("stream pipeline over image chunks" if chunked
-                          else "separate kernels (hist | solve + LUT | apply)"),
+            "path": path_name,
             "fused_ms": {"zero": round(st0, 4), "k_fused": round(st1, 4)} if fused else None,
             "stages_ms" if not (fused or chunked) else "stages_ms_unfused_info":
                          {"hist": round(hist_ms, 4), "solve": round(solve_ms, 4), "apply": round(apply_ms, 4),

@@ -146,7 +146,9 @@ hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_de
 /* Steps (1)-(4) for the whole batch ("matching its histogram with the one provided by
    HistRetinex") on `stream`.  Default: the histogram, solve + LUT and apply kernels in order,
    chained by programmatic dependent launch, the apply acquiring each image's LUT-ready flag
-   (so it overlaps the solver's tail).  Policy (hr_set_policy): for fused_min_b <= B <=
+   (so it overlaps the solver's tail); for 2 <= B <= #SMs / 2 the grouped step (two image
+   groups, policy "groups": the second group's histograms run beside the first group's solves,
+   the apply beside the second group's solves).  Policy (hr_set_policy): for fused_min_b <= B <=
    fused_max_b (fused_min_b = 0 = off by default) with 16-byte aligned buffers and
    H*W % 16 == 0, ONE persistent kernel runs the
    histograms, each image's solve + LUT as soon as its histograms are complete, and the
@@ -226,10 +228,21 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
      "apply_dyn"    separate kernels: 1 = the apply takes images in the order     default 0
                     their LUTs complete (completion queue filled by the solver);
                     2 = natural order after the solver grid; both with per-warp
-                    tickets of apply_gs chunks that balance the streaming work
+                    tickets of apply_gs chunks that balance the streaming work;
+                    3 = first half of the images split statically, second half
+                    by CTA tickets, gated by the per-image LUT-ready flags
      "apply_gs"     1024-pixel chunks per dynamic-apply warp ticket (>= 1)      default 8
      "hist_overlap" separate kernels: each solver CTA starts when its image's  default 0
                     histogram segments are flushed (histograms at 2x256 threads per SM)
+     "groups"       grouped step (>= 2): images in G groups, launched in order  default -1
+                    hist(0) solve(0) hist(1) solve(1) ... solve(G-1) apply; the
+                    histograms of group k+1 run beside the solves of group k (they
+                    do not wait for them), the apply (every CTA: groups 0..G-2
+                    first) beside the last group's solves; streaming grids sized
+                    to the slots the resident solver CTAs leave.  0/1: off;
+                    -1: auto = 2 when 2 <= B <= #SMs / 2, else off
+     "group_apply"  grouped step's apply: 0 static shares (groups 0..G-2, then     default 0
+                    the last group); 1 the last group by CTA tickets
      "hist_tma"     histogram kernel with TMA-staged rows (one CTA per SM; in     default 0
                     the hist_overlap form 512 threads in image waves) for 16-B
                     aligned batches with W % 16 == 0 (256 <= W <= 8192) or
@@ -237,14 +250,17 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
    The environment variables HR_<KEY upper-cased> set the initial values at hr_create.
    Returns HR_EINVAL for an unknown key or an out-of-range value (nothing changes). */
 hr_status hr_set_policy(hr_ctx* ctx, const char* key, int64_t value);
+/* Current value of a policy key (same keys as hr_set_policy) into *value.  HR_EINVAL for a
+   NULL ctx / key / value or an unknown key (*value untouched). */
+hr_status hr_get_policy(hr_ctx* ctx, const char* key, int64_t* value);
 
 /* Number of CUDA kernels this context has launched so far (all entry points, including the
    accumulator-zeroing kernel; driver memsets are not counted).  -1 for a NULL ctx. */
 int64_t hr_kernel_launches(const hr_ctx* ctx);
 
 /* Execution path of the last hr_enhance on this context: 0 separate kernels (histogram |
-   solve + LUT | apply), 1 the persistent fused kernel, 2 the chunk pipeline; -1 none yet or
-   a NULL ctx. */
+   solve + LUT | apply), 1 the persistent fused kernel, 2 the chunk pipeline, 3 the grouped
+   step (policy "groups"); -1 none yet or a NULL ctx. */
 int32_t hr_last_path(const hr_ctx* ctx);
 
 #ifdef __cplusplus

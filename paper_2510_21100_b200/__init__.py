@@ -231,6 +231,15 @@ def set_policy(key: str, value: int, device=None) -> None:
     _check(_lib.load().hr_set_policy(ctx, key.encode(), int(value)), ctx)
 
 
+def get_policy(key: str, device=None) -> int:
+    """hr_get_policy: current value of an hr_enhance policy key on `device`."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    ctx = _context(dev)
+    v = ctypes.c_int64(0)
+    _check(_lib.load().hr_get_policy(ctx, key.encode(), ctypes.byref(v)), ctx)
+    return int(v.value)
+
+
 def hr_enhance_host(rgb_host: torch.Tensor, params: Params | None = None, out_host: torch.Tensor | None = None,
                     device=None, chunks: int = 0, in_dev: torch.Tensor | None = None,
                     out_dev: torch.Tensor | None = None, workspace: torch.Tensor | None = None,

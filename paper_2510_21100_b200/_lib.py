@@ -20,7 +20,7 @@ EXPORTS = (
     "hr_version", "hr_workspace_bytes", "hr_histogram", "hr_solve", "hr_match", "hr_apply",
     "hr_enhance", "hr_enhance_debug", "hr_profile_enable", "hr_profile_collect", "hr_set_policy",
     "hr_kernel_launches", "hr_enhance_host", "hr_last_path", "hr_solve_trace", "hr_he",
-    "hr_quality_workspace_bytes", "hr_quality",
+    "hr_quality_workspace_bytes", "hr_quality", "hr_get_policy",
 )
 
 
@@ -81,6 +81,7 @@ def load() -> ctypes.CDLL:
         "hr_profile_enable": ([vp, i32], i32),
         "hr_profile_collect": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)], i32),
         "hr_set_policy": ([vp, ctypes.c_char_p, i64], i32),
+        "hr_get_policy": ([vp, ctypes.c_char_p, ctypes.POINTER(i64)], i32),
         "hr_kernel_launches": ([vp], i64),
         "hr_last_path": ([vp], i32),
         "hr_he": ([vp, vp, i64, i32, i32, vp, vp, vp, vp], i32),

@@ -57,6 +57,31 @@ __device__ __forceinline__ void load_strip(const uint8_t* __restrict__ p, uint32
       w[4 * i + 2] = a.z;
       w[4 * i + 3] = a.w;
     }
+  } else if constexpr (VEC == 9) {
+    // 8-B aligned rows whose 16-B alignment alternates (3 W % 16 == 8): 16-B aligned -> three
+    // 16-B loads; 8 mod 16 -> 8 + 16 + 16 + 8 B (4 loads instead of the six 8-B loads).  The
+    // branch is warp-uniform: every lane of a step reads a row of the same parity (RPG even)
+    static_assert(NWD == 12, "mixed-alignment loads are for 16-px strips");
+    if ((reinterpret_cast<uintptr_t>(p) & 8u) == 0) {
+      const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const uint4 a = __ldg(q + i);
+        w[4 * i] = a.x;
+        w[4 * i + 1] = a.y;
+        w[4 * i + 2] = a.z;
+        w[4 * i + 3] = a.w;
+      }
+    } else {
+      const uint2 a = __ldg(reinterpret_cast<const uint2*>(p));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(p + 8));
+      const uint4 c = __ldg(reinterpret_cast<const uint4*>(p + 24));
+      const uint2 d = __ldg(reinterpret_cast<const uint2*>(p + 40));
+      w[0] = a.x, w[1] = a.y;
+      w[2] = b.x, w[3] = b.y, w[4] = b.z, w[5] = b.w;
+      w[6] = c.x, w[7] = c.y, w[8] = c.z, w[9] = c.w;
+      w[10] = d.x, w[11] = d.y;
+    }
   } else if constexpr (VEC == 8) {
     const uint2* q = reinterpret_cast<const uint2*>(p);
 #pragma unroll
@@ -156,9 +181,80 @@ __device__ __forceinline__ void hist_zero(uint32_t* sm) {
   for (int i = threadIdx.x; i < kHistWords / 4; i += NT) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
+// One thread's walk down a G-group (4 G px) strip: rows ya .. ya + nr - 1 of the band (+ the
+// halo row when `halo`), starting at p (the strip's first byte in row ya).  rowEnd: the strip's
+// last pixel is x = W - 1 (dx = 0 there, no neighbour load).  RPG + 1 row steps for every lane
+// (a warp-uniform trip count); lanes with nr == 0 only mask their counts.
+template <int G, int VEC>
+__device__ __forceinline__ void walk_strip(const uint8_t* __restrict__ p, size_t rowBytes, int RPG, int nr,
+                                           bool halo, bool rowEnd, uint32_t sb, uint32_t* ghi, uint32_t Lv,
+                                           uint32_t Lg) {
+  uint32_t Vp[G], Dp[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) Vp[q] = Dp[q] = 0u;
+  auto need = [&](int it) { return it < nr || (it == nr && halo); };  // row ya+it is read
+  auto load_row = [&](const uint8_t* pr, uint32_t (&wr)[3 * G], uint32_t& nbr) {
+    if constexpr (G == 4) {
+      load_strip<16, VEC>(pr, wr);
+    } else {  // half strip (8 px, 24 B, 8-B aligned)
+      static_assert(G == 2, "");
+      const uint2* q = reinterpret_cast<const uint2*>(pr);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const uint2 a = __ldg(q + i);
+        wr[2 * i] = a.x;
+        wr[2 * i + 1] = a.y;
+      }
+    }
+    nbr = rowEnd ? 0u : load_nb<VEC>(pr + 12 * G);
+  };
+  // step it: row ya+it -> value channel, H_C(S) counts, dx; gradient of row ya+it-1
+  auto step = [&](const uint32_t (&wr)[3 * G], uint32_t nbr, int it) {
+    uint32_t Vc[G], Dc[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) Vc[q] = value4(wr[3 * q], wr[3 * q + 1], wr[3 * q + 2]);
+    if (it < nr) {  // H_C(S), Eq. 3
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        sinc(sb, __byte_perm(Lv, Vc[q], 0x1140u));
+        sinc(sb, __byte_perm(Lv, Vc[q], 0x1150u));
+        sinc(sb, __byte_perm(Lv, Vc[q], 0x1160u));
+        sinc(sb, __byte_perm(Lv, Vc[q], 0x1170u));
+      }
+    }
+    const uint32_t nbV = nb_value<VEC>(nbr);
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+      Dc[q] = __vabsdiffu4(Vc[q], __funnelshift_r(Vc[q], q < G - 1 ? Vc[q + 1] : nbV, 8));
+    if (rowEnd) Dc[G - 1] &= 0x00FFFFFFu;  // dx = 0 at x = W-1
+    if (it > 0 && it <= nr) grad_row<G>(sb, ghi, Lg, Dp, Vp, Vc, it < nr || halo);  // dy = 0 on the last row
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      Vp[q] = Vc[q];
+      Dp[q] = Dc[q];
+    }
+  };
+  // two register sets alternate: row it+1 is in flight while row it is processed
+  uint32_t wa[3 * G], wb[3 * G], na = 0u, nb = 0u;
+#pragma unroll
+  for (int i = 0; i < 3 * G; ++i) wa[i] = wb[i] = 0u;
+  if (need(0)) load_row(p, wa, na);
+  for (int it = 0; it <= RPG; it += 2) {
+    if (need(it + 1)) load_row(p + rowBytes, wb, nb);
+    step(wa, na, it);
+    if (it + 1 > RPG) break;
+    if (need(it + 2)) load_row(p + 2 * rowBytes, wa, na);
+    step(wb, nb, it + 1);
+    p += 2 * rowBytes;
+  }
+}
+
 // Histogram rows [y0, y1) of one H x W image `img` into the (zeroed) lane-private counters
 // `sm`, then flush them with integer atomics into hist_s_b[256] / hist_graw_b[512].  All NT
 // threads call it; it ends with a barrier (the counters are then free for reuse, not zero).
+// W % 16 == 8 with 8-B aligned rows (VEC 8/9): the last 8 columns of each row are "half strips"
+// walked by their own threads, placed in warps of their own (from the first multiple of 32 past
+// the full-strip threads) so neither kind of warp diverges; one row group fewer when needed.
 template <int SW, int VEC, int NT>
 __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, int H, int W, int y0, int y1,
                                              uint32_t* sm, uint32_t* __restrict__ hist_s_b,
@@ -172,9 +268,15 @@ __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, in
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
 
   const int SPf = W / SW;   // full strips per row
-  const int xt = SPf * SW;  // first column of the scalar tail
+  int xt = SPf * SW;        // first column of the scalar tail
   const int SPt = SPf < NT ? SPf : NT;
-  const int NG = SPf == 0 ? 0 : (SPf < NT ? NT / SPf : 1);  // row groups
+  int NG = SPf == 0 ? 0 : (SPf < NT ? NT / SPf : 1);  // row groups
+  const bool half = SW == 16 && (VEC == 8 || VEC == 9) && W - xt == 8 && SPf > 0 && SPf < NT;
+  if (half)
+    while (NG > 1 && ((NG * SPf + 31) & ~31) + NG > NT) --NG;
+  const int TH = ((NG * SPf + 31) & ~31);  // first half-strip thread
+  const bool halfOk = half && TH + NG <= NT;
+  if (halfOk) xt = W;  // no scalar tail
   const int ntile = (SPf + NT - 1) / NT;
   const int grp = SPt ? tid / SPt : 0;
   const int sl = SPt ? tid - grp * SPt : 0;
@@ -186,65 +288,28 @@ __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, in
   // y+1 is loaded before row y is processed, so two rows of loads are in flight per thread.
   if (NG > 0) {
     const int nrows = y1 - y0;
-    const int RPG = (nrows + NG - 1) / NG;
-    const int ya = y0 + grp * RPG;
-    const int yb = min(y1, ya + RPG);
-    for (int tile = 0; tile < ntile; ++tile) {
-      const int s = tile * NT + sl;
-      // every lane runs the same RPG + 1 row steps (warp-uniform trip count); lanes past their
-      // band's end, or without a strip, only mask their counts
-      const bool act = (grp < NG) && (s < SPf) && (ya < yb);
-      const int nr = act ? yb - ya : 0;  // rows of this thread's band
-      const bool halo = act && yb < H;   // row yb exists: the gradient of row yb-1 needs it
-      const int x0 = act ? s * SW : 0;
-      const bool rowEnd = (s == SPf - 1) && (xt == W);  // last pixel of this strip is x = W-1
-      const uint8_t* p = img + (size_t)(act ? ya : 0) * rowBytes + (size_t)x0 * 3;
-      uint32_t Vp[G], Dp[G];
-#pragma unroll
-      for (int q = 0; q < G; ++q) Vp[q] = Dp[q] = 0u;
-      auto need = [&](int it) { return it < nr || (it == nr && halo); };  // row ya+it is read
-      auto load_row = [&](const uint8_t* pr, uint32_t (&wr)[3 * G], uint32_t& nbr) {
-        load_strip<SW, VEC>(pr, wr);
-        nbr = rowEnd ? 0u : load_nb<VEC>(pr + 3 * SW);
-      };
-      // step it: row ya+it -> value channel, H_C(S) counts, dx; gradient of row ya+it-1
-      auto step = [&](const uint32_t (&wr)[3 * G], uint32_t nbr, int it) {
-        uint32_t Vc[G], Dc[G];
-#pragma unroll
-        for (int q = 0; q < G; ++q) Vc[q] = value4(wr[3 * q], wr[3 * q + 1], wr[3 * q + 2]);
-        if (it < nr) {  // H_C(S), Eq. 3
-#pragma unroll
-          for (int q = 0; q < G; ++q) {
-            sinc(sb, __byte_perm(Lv, Vc[q], 0x1140u));
-            sinc(sb, __byte_perm(Lv, Vc[q], 0x1150u));
-            sinc(sb, __byte_perm(Lv, Vc[q], 0x1160u));
-            sinc(sb, __byte_perm(Lv, Vc[q], 0x1170u));
-          }
-        }
-        const uint32_t nbV = nb_value<VEC>(nbr);
-#pragma unroll
-        for (int q = 0; q < G; ++q)
-          Dc[q] = __vabsdiffu4(Vc[q], __funnelshift_r(Vc[q], q < G - 1 ? Vc[q + 1] : nbV, 8));
-        if (rowEnd) Dc[G - 1] &= 0x00FFFFFFu;  // dx = 0 at x = W-1
-        if (it > 0 && it <= nr) grad_row<G>(sb, ghi, Lg, Dp, Vp, Vc, it < nr || halo);  // dy = 0 on the last row
-#pragma unroll
-        for (int q = 0; q < G; ++q) {
-          Vp[q] = Vc[q];
-          Dp[q] = Dc[q];
-        }
-      };
-      // two register sets alternate: row it+1 is in flight while row it is processed
-      uint32_t wa[3 * G], wb[3 * G], na = 0u, nb = 0u;
-#pragma unroll
-      for (int i = 0; i < 3 * G; ++i) wa[i] = wb[i] = 0u;
-      if (need(0)) load_row(p, wa, na);
-      for (int it = 0; it <= RPG; it += 2) {
-        if (need(it + 1)) load_row(p + rowBytes, wb, nb);
-        step(wa, na, it);
-        if (it + 1 > RPG) break;
-        if (need(it + 2)) load_row(p + 2 * rowBytes, wa, na);
-        step(wb, nb, it + 1);
-        p += 2 * rowBytes;
+    int RPG = (nrows + NG - 1) / NG;
+    if constexpr (VEC == 9) RPG += RPG & 1;  // even: the rows of one step share their parity
+    if (halfOk && tid >= TH) {  // half-strip walkers (whole warps of them, or idle)
+      const int g = tid - TH;
+      const int ya = y0 + g * RPG;
+      const int yb = min(y1, ya + RPG);
+      const bool act = g < NG && ya < yb;
+      const int nr = act ? yb - ya : 0;
+      const uint8_t* p = img + (size_t)(act ? ya : 0) * rowBytes + (size_t)(SPf * SW) * 3;
+      walk_strip<2, VEC>(p, rowBytes, RPG, nr, act && yb < H, true, sb, ghi, Lv, Lg);
+    } else {
+      for (int tile = 0; tile < ntile; ++tile) {
+        const int s = tile * NT + sl;
+        const bool act = (grp < NG) && (s < SPf) && (y0 + grp * RPG < min(y1, y0 + grp * RPG + RPG));
+        const int ya = y0 + grp * RPG;
+        const int yb = min(y1, ya + RPG);
+        const int nr = act ? yb - ya : 0;  // rows of this thread's band
+        const bool halo = act && yb < H;   // row yb exists: the gradient of row yb-1 needs it
+        const int x0 = act ? s * SW : 0;
+        const bool rowEnd = (s == SPf - 1) && (xt == W) && !halfOk;  // last pixel of this strip is x = W-1
+        const uint8_t* p = img + (size_t)(act ? ya : 0) * rowBytes + (size_t)x0 * 3;
+        walk_strip<G, VEC>(p, rowBytes, RPG, nr, halo, rowEnd, sb, ghi, Lv, Lg);
       }
     }
   }

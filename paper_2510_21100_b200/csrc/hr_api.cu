@@ -35,13 +35,18 @@ struct hr_ctx {
   int solve_cpsm = 0;     // k_solve CTAs per SM: 1, 2, or 0 = auto (1 when B <= SMs)
   int apply_gs = 8;       // dynamic apply: 1024-px chunks per warp ticket
   int apply_dyn = 0;      // separate kernels: 1 = the apply takes images in LUT-completion order,
-                          // 2 = natural order after the solver grid, warp tickets balancing the work
+                          // 2 = natural order after the solver grid, 3 = natural order gated by the
+                          // per-image LUT-ready flags; warp tickets balancing the work
                           // (off: per-warp tickets scatter the streams; C3 0.364 vs 0.269 ms)
   int hist_tma = 0;       // k_hist: TMA-staged rows where the shape allows (off: measured no faster)
   int hist_overlap = 0;   // separate kernels: solves start per image beside a 2x256-thread histogram pass
                           // (off: the 16-warp histogram pass costs more than the overlap saves)
+  int group_apply = 0;    // grouped step's apply: 0 = static shares of groups 0..G-2, then of the
+                          // last group; 1 = last group by CTA tickets (measured slower)
+  int groups = -1;        // grouped step (>= 2): histograms of group k+1 run beside the solves of
+                          // group k, the apply beside the last group's solves (0/1: off)
   int64_t launches = 0;   // kernels launched through this context (hr_kernel_launches)
-  int last_path = -1;     // hr_last_path: 0 separate kernels, 1 fused, 2 chunk pipeline
+  int last_path = -1;     // hr_last_path: 0 separate kernels, 1 fused, 2 chunk pipeline, 3 grouped
   cudaStream_t sH = nullptr, sS = nullptr, sA = nullptr;
   std::vector<cudaEvent_t> pev;  // pipeline events
   cudaStream_t sIn = nullptr, sOut = nullptr;  // hr_enhance_host copy streams
@@ -207,8 +212,10 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_SOLVE_CPSM")) c->solve_cpsm = atoi(v) >= 0 && atoi(v) <= 2 ? atoi(v) : 0;
   if (const char* v = getenv("HR_HIST_OVERLAP")) c->hist_overlap = atoi(v) != 0;
   if (const char* v = getenv("HR_HIST_TMA")) c->hist_tma = atoi(v) != 0;
-  if (const char* v = getenv("HR_APPLY_DYN")) c->apply_dyn = atoi(v) >= 0 && atoi(v) <= 2 ? atoi(v) : 0;
+  if (const char* v = getenv("HR_APPLY_DYN")) c->apply_dyn = atoi(v) >= 0 && atoi(v) <= 3 ? atoi(v) : 0;
   if (const char* v = getenv("HR_APPLY_GS")) c->apply_gs = atoi(v) > 0 ? atoi(v) : 8;
+  if (const char* v = getenv("HR_GROUP_APPLY")) c->group_apply = atoi(v) != 0;
+  if (const char* v = getenv("HR_GROUPS")) c->groups = atoi(v) >= -1 && atoi(v) <= 64 ? atoi(v) : -1;
   *out = c;
   return HR_OK;
 }
@@ -240,14 +247,14 @@ hr_status hr_profile_enable(hr_ctx* c, int32_t on) {
 int64_t hr_kernel_launches(const hr_ctx* c) { return c ? c->launches : -1; }
 int32_t hr_last_path(const hr_ctx* c) { return c ? c->last_path : -1; }
 
-hr_status hr_set_policy(hr_ctx* c, const char* key, int64_t v) {
-  if (!c) return HR_EINVAL;
-  if (!key) return set_err(c, HR_EINVAL, "NULL key");
-  struct Knob {
-    const char* name;
-    int* field;
-    int64_t lo, hi;
-  };
+namespace {
+struct Knob {
+  const char* name;
+  int* field;
+  int64_t lo, hi;
+};
+// the policy knob named key (nullptr if unknown)
+const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
   const Knob knobs[] = {
       {"fused_min_b", &c->fused_min_b, 0, 1 << 30}, {"fused_max_b", &c->fused_max_b, 0, 1 << 30},
       {"fused_cpsm", &c->fused_cpsm, 1, 2},
@@ -255,15 +262,36 @@ hr_status hr_set_policy(hr_ctx* c, const char* key, int64_t v) {
       {"chunks", &c->chunks, 1, 1 << 16},           {"hist_cpsm", &c->hist_cpsm, 1, 2},
       {"apply_cpsm", &c->apply_cpsm, 1, 2},         {"warp_solver", &c->warp_solver, 0, 1},
       {"solve_cpsm", &c->solve_cpsm, 0, 2},         {"hist_overlap", &c->hist_overlap, 0, 1},
-      {"apply_dyn", &c->apply_dyn, 0, 2},           {"apply_gs", &c->apply_gs, 1, 1 << 20},           {"hist_tma", &c->hist_tma, 0, 1},
+      {"apply_dyn", &c->apply_dyn, 0, 3},           {"apply_gs", &c->apply_gs, 1, 1 << 20},
+      {"hist_tma", &c->hist_tma, 0, 1},             {"groups", &c->groups, -1, 64},
+      {"group_apply", &c->group_apply, 0, 1},
   };
-  for (const Knob& k : knobs) {
-    if (strcmp(k.name, key) != 0) continue;
-    if (v < k.lo || v > k.hi) return set_err(c, HR_EINVAL, "policy value out of range");
-    *k.field = (int)v;
-    return HR_OK;
-  }
-  return set_err(c, HR_EINVAL, "unknown policy key");
+  for (const Knob& k : knobs)
+    if (strcmp(k.name, key) == 0) {
+      *out = k;
+      return out;
+    }
+  return nullptr;
+}
+}  // namespace
+
+hr_status hr_set_policy(hr_ctx* c, const char* key, int64_t v) {
+  if (!c) return HR_EINVAL;
+  if (!key) return set_err(c, HR_EINVAL, "NULL key");
+  Knob k;
+  if (!find_knob(c, key, &k)) return set_err(c, HR_EINVAL, "unknown policy key");
+  if (v < k.lo || v > k.hi) return set_err(c, HR_EINVAL, "policy value out of range");
+  *k.field = (int)v;
+  return HR_OK;
+}
+
+hr_status hr_get_policy(hr_ctx* c, const char* key, int64_t* value) {
+  if (!c) return HR_EINVAL;
+  if (!key || !value) return set_err(c, HR_EINVAL, "NULL key or value");
+  Knob k;
+  if (!find_knob(c, key, &k)) return set_err(c, HR_EINVAL, "unknown policy key");
+  *value = *k.field;
+  return HR_OK;
 }
 
 hr_status hr_profile_collect(hr_ctx* c, double* stage_ms, int32_t* steps) {
@@ -444,7 +472,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   };
   auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, uint32_t* ready = nullptr,
                          const uint32_t* hist_done = nullptr, int hist_bands = 0, uint32_t* queue = nullptr,
-                         uint32_t* queue_tail = nullptr) -> cudaError_t {
+                         uint32_t* queue_tail = nullptr, int cpsm = 0) -> cudaError_t {
     hr::SolveArgs a{};
     a.ready = c->warp_solver ? nullptr : ready;
     a.queue = c->warp_solver ? nullptr : queue;
@@ -470,7 +498,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       return r;
     }
     a.lut = lut + b0 * kLevels;  // CDF + LUT tail fused into the solver CTA (no target round trip)
-    return counted(c, hr::launch_solve(a, nb, hist_done ? 2 : solve_cpsm_for(c, nb), s));
+    return counted(c, hr::launch_solve(a, nb, hist_done ? 2 : cpsm ? cpsm : solve_cpsm_for(c, nb), s));
   };
   auto apply_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, const uint32_t* ready = nullptr) -> cudaError_t {
     return counted(c, hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s,
@@ -510,6 +538,59 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     if (e == cudaSuccess) e = counted(c, hr::launch_fused(f, grid, st));
     c->last_path = 1;
     if (e == cudaSuccess) e = mark(2);
+    if (e == cudaSuccess) e = mark(3);
+    return cuda_err(c, e, "hr_enhance");
+  }
+  // grouped step: images in G groups; one stream, every kernel launched early (programmatic
+  // dependent launch):  zero | hist(0) | solve(0) | hist(1) | solve(1) | ... | solve(G-1) | apply.
+  // No kernel after hist(0) waits for its predecessor grid (griddepcontrol.wait waits for
+  // everything earlier in the stream, which would serialise the solves): hist(k), k >= 1, shares
+  // no data with solve(k-1), so the streaming pass runs on the slots the earlier solves leave
+  // free; each solver CTA acquires its image's flushed-row count (all H rows: histograms
+  // complete); the apply acquires each image's LUT-ready flag and takes every CTA's share
+  // of groups 0..G-2 before its share of group G-1, so it overlaps the last solves.  The
+  // streaming grids are sized to the slots left beside the resident solver CTAs (a solver CTA
+  // takes one streaming CTA's registers).
+  const bool ready_ok = [] {
+    const char* v = getenv("HR_READY");
+    return !(v && atoi(v) == 0);
+  }();
+  // groups < 0 (default): 2 groups when B <= SMs / 2 (each group's solves then take at most a
+  // quarter of the CTA slots; C3 0.263 vs 0.270 ms), else off (C5, 256 images: 0.193 vs 0.176)
+  const int ngroups = c->groups >= 0 ? c->groups : (B >= 2 && B <= c->num_sms / 2 ? 2 : 0);
+  if (ngroups >= 2 && B >= 2 && !c->warp_solver && ready_ok) {
+    const int64_t G = std::min<int64_t>(ngroups, B);
+    uint32_t* ctl = reinterpret_cast<uint32_t*>((char*)ws + L.ctl);
+    uint32_t* done = ctl + hr::kCtlHeader;  // rows flushed per image (k_hist -> k_solve)
+    uint32_t* ready = ctl + hr::kCtlHeader + B;
+    c->last_path = 3;
+    if (e == cudaSuccess) e = mark(0);
+    if (e == cudaSuccess) e = counted(c, hr::launch_zero(hs, (size_t)B * kLevels * sizeof(uint32_t), st));
+    if (e == cudaSuccess) e = counted(c, hr::launch_zero(graw, (size_t)B * kGradSlots * sizeof(uint32_t), st));
+    if (e == cudaSuccess) e = counted(c, hr::launch_zero((char*)ws + L.ctl, align_up(hr::fused_ctl_bytes(B)), st));
+    if (e == cudaSuccess) e = mark(1);
+    const int slots = hist_grid(c);
+    int64_t prev_nb = 0;
+    for (int64_t k = 0; k < G && e == cudaSuccess; ++k) {
+      const int64_t b0 = B * k / G, nb = B * (k + 1) / G - b0;
+      const int grid = (int)std::max<int64_t>(c->num_sms, slots - std::min<int64_t>(prev_nb, slots / 2));
+      e = counted(c, hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, grid, st,
+                                     hr::kHistThreads, done + b0, 0, k > 0));
+      if (e == cudaSuccess) e = solve_chunk(b0, nb, st, ready + b0, done + b0, 0, nullptr, nullptr, 2);
+      prev_nb = nb;
+    }
+    if (e == cudaSuccess) e = mark(2);
+    static const int ag_sub = [] {  // measurement switch: apply slots given up per last-group solve
+      const char* v = getenv("HR_GROUP_AG_SUB");
+      return v ? atoi(v) : 1;
+    }();
+    const int ag = (int)std::max<int64_t>(c->num_sms, apply_grid(c) - std::min<int64_t>(ag_sub * prev_nb, apply_grid(c) / 2));
+    const int64_t b_last = B * (G - 1) / G;
+    if (e == cudaSuccess)
+      e = c->group_apply == 1 && hr::apply_dyn_supported(in, out, B, H, W)
+              ? counted(c, hr::launch_apply_dyn(in, lut, B, H, W, out, ag, nullptr, ctl + 3, c->apply_gs, st, ready,
+                                                b_last))
+              : counted(c, hr::launch_apply(in, lut, B, H, W, out, ag, st, ready, b_last));
     if (e == cudaSuccess) e = mark(3);
     return cuda_err(c, e, "hr_enhance");
   }
@@ -560,7 +641,8 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
                       queue ? ctl + 2 : nullptr);
     if (e == cudaSuccess) e = mark(2);
     if (e == cudaSuccess)
-      e = dyn ? counted(c, hr::launch_apply_dyn(in, lut, B, H, W, out, apply_grid(c), queue, ctl + 3, c->apply_gs, st))
+      e = dyn ? counted(c, hr::launch_apply_dyn(in, lut, B, H, W, out, apply_grid(c), queue, ctl + 3, c->apply_gs, st,
+                                                c->apply_dyn == 3 ? ready : nullptr, c->apply_dyn == 3 ? B / 2 : 0))
               : apply_chunk(0, B, st, ready);
     if (e == cudaSuccess) e = mark(3);
     return cuda_err(c, e, "hr_enhance");

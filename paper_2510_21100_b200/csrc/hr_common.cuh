@@ -151,7 +151,10 @@ constexpr int kApplyThreads = 256;
 // (hist_wave_images), leaving registers and shared memory for one solver CTA per SM
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
                         uint32_t* hist_graw, int grid, cudaStream_t st, int nt = kHistThreads,
-                        uint32_t* done = nullptr, int tma = 1);
+                        uint32_t* done = nullptr, int tma = 1, bool nowait = false);
+// nowait: the kernel does not wait for its stream predecessor (griddepcontrol.wait); only for a
+// predecessor it shares no data with (the grouped step's histograms of group k >= 1 follow the
+// solver of group k - 1)
 int hist_grid_clamped(int64_t B, int32_t H, int grid);  // the grid launch_hist actually uses
 bool tma_hist_supported(const uint8_t* rgb, int64_t B, int32_t H, int32_t W);
 // Wave order of the TMA histogram kernel with per-image completion counts: images
@@ -204,12 +207,18 @@ cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B
 // ready (nullable): per-image LUT-ready flags released by k_solve; when given, the TMA apply
 // does not wait for the solver grid to finish but acquires ready[b] before image b's table
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
-                         uint8_t* out, int grid_ctas, cudaStream_t st, const uint32_t* ready = nullptr);
+                         uint8_t* out, int grid_ctas, cudaStream_t st, const uint32_t* ready = nullptr,
+                         int64_t b_last = 0);
+// b_last (0 < b_last < B): every CTA first takes its share of images [0, b_last), then its share
+// of [b_last, B) (the grouped step: the last group's LUTs complete last)
 // dynamic apply: warps take groups of GS chunks of the images in LUT-completion order (queue
 // filled by k_solve); false when the shape needs the scalar path (then use launch_apply)
 bool apply_dyn_supported(const uint8_t* in, const uint8_t* out, int64_t B, int32_t H, int32_t W);
 cudaError_t launch_apply_dyn(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
-                             int grid_ctas, const uint32_t* queue, uint32_t* ticket, int GS, cudaStream_t st);
+                             int grid_ctas, const uint32_t* queue, uint32_t* ticket, int GS, cudaStream_t st,
+                             const uint32_t* ready = nullptr, int64_t b_last = 0);
+// (ready given, queue NULL, 0 < b_last < B: images [0, b_last) split statically per CTA, images
+// [b_last, B) by tickets)
 // second workload (k_quality.cu): HE LUT per image (Eq. 4-5) and the quality metrics
 cudaError_t launch_he_lut(const uint32_t* hist_s, int64_t B, uint8_t* lut, cudaStream_t st);
 size_t quality_ws_bytes(int64_t B, int32_t H, int32_t W);

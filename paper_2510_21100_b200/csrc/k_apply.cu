@@ -27,7 +27,7 @@ namespace {
 
 __global__ void __launch_bounds__(kApplyThreads, 2)
 k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int64_t B, int64_t HW,
-            uint8_t* __restrict__ out, const uint32_t* __restrict__ ready) {
+            uint8_t* __restrict__ out, const uint32_t* __restrict__ ready, int64_t b_last) {
   extern __shared__ __align__(128) unsigned char smraw[];
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -41,36 +41,38 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   __syncthreads();
 
   const uint32_t cpi = (uint32_t)((HW + kChunkPx - 1) / kChunkPx);  // chunks per image
-  const int64_t G = B * (int64_t)cpi;                               // < 2^31 (host-checked)
-  const uint32_t g0 = (uint32_t)(G * blockIdx.x / gridDim.x), g1 = (uint32_t)(G * (blockIdx.x + 1) / gridDim.x);
-  // this warp's chunks: g0 + w, g0 + w + kWarps, ...
-  const int mine = (g1 - g0 > (uint32_t)w) ? (int)((g1 - g0 - w + kWarps - 1) / kWarps) : 0;
+  // chunk space in two parts: images [0, b_last) then [b_last, B) (b_last = B: one part); this
+  // CTA takes a contiguous share of each part, part A first
+  if (b_last <= 0 || b_last > B) b_last = B;
+  const uint32_t GA = (uint32_t)(b_last * (int64_t)cpi), GB = (uint32_t)(B * (int64_t)cpi) - GA;  // < 2^31
+  const uint32_t a0 = (uint32_t)((uint64_t)GA * blockIdx.x / gridDim.x), a1 = (uint32_t)((uint64_t)GA * (blockIdx.x + 1) / gridDim.x);
+  const uint32_t c0 = GA + (uint32_t)((uint64_t)GB * blockIdx.x / gridDim.x);
+  const uint32_t c1 = GA + (uint32_t)((uint64_t)GB * (blockIdx.x + 1) / gridDim.x);
+  // this warp's chunks: a0 + w, a0 + w + kWarps, ... < a1, then c0 + w, ... < c1
+  auto cnt = [&](uint32_t lo, uint32_t hi) { return (hi - lo > (uint32_t)w) ? (int)((hi - lo - w + kWarps - 1) / kWarps) : 0; };
+  const int nA = cnt(a0, a1);
+  const int mine = nA + cnt(c0, c1);
   const uint64_t pol = policy_evict_first();
   uint2* tab = s.tab[w];
   int64_t cur_img = -1;
 
-  // chunk cursor: image b, chunk c within the image; advances by kWarps chunks
+  // chunk cursor: image b, chunk c within the image; i = this warp's chunk ordinal
   struct Cur {
     uint32_t b, c;
+    int i;
   };
-  auto start = [&]() {
-    const uint32_t g = g0 + (uint32_t)w;
-    return Cur{g / cpi, g % cpi};
+  auto at = [&](int i) {
+    const uint32_t g = i < nA ? a0 + (uint32_t)w + (uint32_t)i * kWarps : c0 + (uint32_t)w + (uint32_t)(i - nA) * kWarps;
+    return Cur{g / cpi, g % cpi, i};
   };
-  auto advance = [&](Cur& k) {
-    k.c += kWarps;
-    while (k.c >= cpi) {
-      k.c -= cpi;
-      ++k.b;
-    }
-  };
+  auto advance = [&](Cur& k) { k = at(k.i + 1); };
   auto where = [&](const Cur& k, uint64_t& off, uint32_t& bytes) {
     const uint32_t px0 = k.c * kChunkPx;
     const uint32_t npx = min((uint32_t)kChunkPx, (uint32_t)(HW - px0));
     off = ((uint64_t)k.b * (uint64_t)HW + px0) * 3u;
     bytes = npx * 3u;
   };
-  Cur ld = start(), cp = ld;  // load cursor (lane 0) and compute cursor
+  Cur ld = at(0), cp = ld;  // load cursor (lane 0) and compute cursor
   auto issue = [&](int i) {
     uint64_t off;
     uint32_t bytes;
@@ -136,18 +138,30 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
 // whatever their start times (CTAs that become resident late take fewer tickets).  Each new image's LUT is loaded into registers when its first chunk is issued
 // (kAhead chunks before it is computed).  Deadlock-free: launched (PDL) only once every solver
 // CTA is resident, and each solve fills one queue slot.
+struct DynSmem {
+  static constexpr int kRing = 4;
+  uint2 meta[kWarps][kStages];
+  uint32_t ring_t[kRing];
+  int ring_tag[kRing], ring_read[kWarps], ring_claim;
+};
+
 __global__ void __launch_bounds__(kApplyThreads, 2)
 k_apply_dyn(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int64_t B, int64_t HW,
-            uint8_t* __restrict__ out, const uint32_t* __restrict__ queue, uint32_t* __restrict__ ticket, uint32_t GS) {
+            uint8_t* __restrict__ out, const uint32_t* __restrict__ queue, uint32_t* __restrict__ ticket, uint32_t GS,
+            const uint32_t* __restrict__ ready, int64_t b_last) {
   extern __shared__ __align__(128) unsigned char smraw[];
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
-  __shared__ uint2 meta[kWarps][kStages];  // (image, chunk) of each stage, image = kEndImg: end
+  // all shared memory is dynamic: a static block before it would push the 128-B aligned
+  // dynamic block to the next 1 KB and leave room for only one CTA per SM
+  DynSmem& x = *reinterpret_cast<DynSmem*>(smraw + sizeof(ApplySmem));
+  auto& meta = x.meta;  // (image, chunk) of each stage, image = kEndImg: end
   constexpr uint32_t kEndImg = 0xFFFFFFFFu;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   TRACE_T0();
-  // with the completion queue there is no grid-wide wait: LUTs arrive through the queue;
-  // without it (natural image order) every LUT is read after the solver grid has completed
-  if (!queue) pdl_wait();
+  // with the completion queue there is no grid-wide wait: LUTs arrive through the queue; with
+  // per-image ready flags (natural order) each image's LUT is acquired before its first group;
+  // with neither every LUT is read after the solver grid has completed
+  if (!queue && !ready) pdl_wait();
   pdl_trigger();
   if (lane == 0) {
     for (int k = 0; k < kStages; ++k) mbar_init(&s.bar[w][k], 1);
@@ -156,22 +170,111 @@ k_apply_dyn(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   __syncthreads();
   const uint32_t cpi = (uint32_t)((HW + kChunkPx - 1) / kChunkPx);
   const uint32_t gpi = (cpi + GS - 1) / GS;
-  const uint64_t ngroups = (uint64_t)B * gpi;
+  // hybrid form (0 < b_last < B, natural order with ready flags): images [0, b_last) are split
+  // statically (this CTA's contiguous share, its warps interleaved chunk by chunk, as in
+  // k_apply_tma) and only images [b_last, B) go by tickets, so CTAs that became resident late
+  // or run slower take fewer of them
+  if (queue || b_last <= 0 || b_last > B) b_last = 0;
+  const uint32_t GA = (uint32_t)(b_last * (int64_t)cpi);
+  const uint32_t a0 = (uint32_t)((uint64_t)GA * blockIdx.x / gridDim.x), a1 = (uint32_t)((uint64_t)GA * (blockIdx.x + 1) / gridDim.x);
+  const uint32_t nA = (a1 - a0 > (uint32_t)w) ? (a1 - a0 - w + kWarps - 1) / kWarps : 0u;
+  uint32_t sA = 0;  // static chunks issued so far
+  const uint64_t ngroups = (uint64_t)(B - b_last) * gpi;
+  // hybrid form, part B: CTA tickets of kWarps * GS contiguous chunks (all warps of the CTA
+  // stream one ticket together, warp w taking chunks w, w + kWarps, ... as in the static part:
+  // per-warp tickets scatter the DRAM streams and measured far slower).  The CTA's k-th ticket
+  // is fetched by the first warp that needs it and published in a ring of kRing slots; a slot
+  // is refilled only after every warp has read its previous ticket (no lag limit otherwise).
+  constexpr int kRing = DynSmem::kRing;
+  uint32_t* ring_t = x.ring_t;
+  int *ring_tag = x.ring_tag, *ring_read = x.ring_read;
+  int& ring_claim = x.ring_claim;
+  const uint32_t GB = (uint32_t)((B - b_last) * (int64_t)cpi), CT = (uint32_t)kWarps * GS;
+  const uint32_t nT = (GB + CT - 1) / CT;
+  if (tid < kRing) ring_tag[tid] = -1;
+  if (tid < kWarps) ring_read[tid] = 0;
+  if (tid == 0) ring_claim = 0;
+  __syncthreads();
+  int tix = -1;           // CTA ticket index this warp is on
+  uint32_t tcur = 0, tm = GS;  // its global ticket, chunks taken from it
+  auto cta_ticket = [&](int i) -> uint32_t {  // lane 0: the CTA's i-th ticket
+    volatile int* tag = ring_tag;
+    volatile uint32_t* rt = ring_t;
+    for (;;) {
+      if (tag[i % kRing] == i) break;
+      if (*(volatile int*)&ring_claim == i && atomicCAS(&ring_claim, i, i + 1) == i) {
+        for (bool ok = false; !ok;) {  // every warp has read ticket i - kRing (slot free)
+          ok = true;
+          for (int u = 0; u < kWarps; ++u) ok = ok && ((volatile int*)ring_read)[u] > i - kRing;
+        }
+        rt[i % kRing] = atomicAdd(ticket, 1u);
+        __threadfence_block();
+        tag[i % kRing] = i;
+        break;
+      }
+      __nanosleep(20);
+    }
+    const uint32_t t = rt[i % kRing];
+    __threadfence_block();
+    ((volatile int*)ring_read)[w] = i + 1;
+    return t;
+  };
   const uint64_t pol = policy_evict_first();
   uint2* tab = s.tab[w];
   // loader state (lane 0): image and chunk range of the current group, prefetched next ticket
-  uint32_t lb = 0, lc = 0, le = 0, nxt = 0;
-  if (lane == 0) nxt = atomicAdd(ticket, 1u);
+  uint32_t lb = 0, lc = 0, le = 0, nxt = 0, rd_img = kEndImg;
+  if (lane == 0 && b_last == 0) nxt = atomicAdd(ticket, 1u);
   auto next_chunk = [&](uint32_t& b, uint32_t& c) -> bool {
+    if (sA < nA) {  // static part
+      const uint32_t g = a0 + (uint32_t)w + sA * kWarps;
+      ++sA;
+      b = g / cpi;
+      c = g - b * cpi;
+      if (ready && b != rd_img) {
+        while (ld_acquire(ready + b) == 0u) __nanosleep(100);
+        rd_img = b;
+      }
+      return true;
+    }
+    if (b_last > 0) {  // part B: CTA tickets
+      for (;;) {
+        if (tm >= GS) {
+          tcur = cta_ticket(++tix);
+          tm = 0;
+        }
+        if (tcur >= nT) {
+          ((volatile int*)ring_read)[w] = 1 << 30;  // never blocks a refill again
+          return false;
+        }
+        const uint32_t g = tcur * CT + (uint32_t)w + tm * kWarps;
+        ++tm;
+        if (g >= GB) {
+          tm = GS;
+          continue;
+        }
+        b = (uint32_t)b_last + g / cpi;
+        c = g % cpi;
+        break;
+      }
+      if (ready && b != rd_img) {
+        while (ld_acquire(ready + b) == 0u) __nanosleep(100);
+        rd_img = b;
+      }
+      return true;
+    }
     if (lc >= le) {
       if (nxt >= ngroups) return false;
-      const uint32_t q = nxt / gpi, g = nxt - q * gpi;
+      const uint32_t q = (uint32_t)b_last + nxt / gpi, g = nxt % gpi;
       if (queue) {
         uint32_t v;
         while ((v = ld_acquire(queue + q)) == 0u) __nanosleep(100);
         lb = v - 1u;
       } else {
         lb = q;
+        if (ready && q != rd_img) {  // natural order gated by the image's LUT-ready flag
+          while (ld_acquire(ready + q) == 0u) __nanosleep(100);
+          rd_img = q;
+        }
       }
       lc = g * GS;
       le = min(lc + GS, cpi);
@@ -298,20 +401,27 @@ bool apply_dyn_supported(const uint8_t* in, const uint8_t* out, int64_t B, int32
 }
 
 cudaError_t launch_apply_dyn(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
-                             int grid_ctas, const uint32_t* queue, uint32_t* ticket, int GS, cudaStream_t st) {
+                             int grid_ctas, const uint32_t* queue, uint32_t* ticket, int GS, cudaStream_t st,
+                             const uint32_t* ready, int64_t b_last) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_apply_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ApplySmem));
+    cudaError_t e = cudaFuncSetAttribute(k_apply_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(ApplySmem) + sizeof(DynSmem)));
+    // the whole carve-out: without it the driver may configure less shared memory than two
+    // CTAs need, halving the resident warps (measured 1.5x slower)
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_apply_dyn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int64_t HW = (int64_t)H * W;
   return launch_pdl(k_apply_dyn, dim3((unsigned)(grid_ctas < 1 ? 1 : grid_ctas)), dim3(kApplyThreads),
-                    sizeof(ApplySmem), st, in, lut, B, HW, out, queue, ticket, (uint32_t)(GS < 1 ? 1 : GS));
+                    sizeof(ApplySmem) + sizeof(DynSmem), st, in, lut, B, HW, out, queue, ticket, (uint32_t)(GS < 1 ? 1 : GS), ready, b_last);
 }
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
-                         int grid_ctas, cudaStream_t st, const uint32_t* ready) {
+                         int grid_ctas, cudaStream_t st, const uint32_t* ready, int64_t b_last) {
   const int64_t HW = (int64_t)H * W;
   const bool tma = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                    (HW % 16 == 0) && B * ((HW + kChunkPx - 1) / kChunkPx) < (1LL << 31);
@@ -331,7 +441,7 @@ cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32
     if (grid > (chunks + kWarps - 1) / kWarps) grid = (chunks + kWarps - 1) / kWarps;
     if (grid < 1) grid = 1;
     return launch_pdl(k_apply_tma, dim3((unsigned)grid), dim3(kApplyThreads), sizeof(ApplySmem), st, in, lut, B, HW,
-                      out, ready);
+                      out, ready, b_last);
   } else {
     int64_t grid = 4LL * grid_ctas;
     const int64_t P = B * HW;

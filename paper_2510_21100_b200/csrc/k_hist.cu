@@ -362,10 +362,10 @@ cudaError_t launch_tma(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint
 template <int SW, int VEC, int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT)
 k_hist(const uint8_t* __restrict__ rgb, int64_t B, int H, int W, uint32_t* __restrict__ hist_s,
-       uint32_t* __restrict__ hist_graw, uint32_t* __restrict__ done) {
+       uint32_t* __restrict__ hist_graw, uint32_t* __restrict__ done, int nowait) {
   extern __shared__ __align__(16) uint32_t sm[];
   TRACE_T0();
-  pdl_wait();
+  if (!nowait) pdl_wait();
   pdl_trigger();
   const int64_t R = B * (int64_t)H;
   const int64_t r_begin = R * blockIdx.x / gridDim.x;
@@ -385,12 +385,12 @@ k_hist(const uint8_t* __restrict__ rgb, int64_t B, int H, int W, uint32_t* __res
       if (threadIdx.x == 0) atomicAdd(done + b, (uint32_t)(y1 - y0));
     }
   }
-  TRACE_END(1u, 0u, 0ull);
+  TRACE_END(1u, (uint32_t)((uintptr_t)hist_s >> 8), 0ull);  // aux: which launch (group)
 }
 
 template <int SW, int VEC, int NT>
 cudaError_t launch_v(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hs, uint32_t* hg, int grid,
-                     uint32_t* done, cudaStream_t st) {
+                     uint32_t* done, cudaStream_t st, bool nowait) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
@@ -398,14 +398,15 @@ cudaError_t launch_v(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(k_hist<SW, VEC, NT>, dim3(grid), dim3(NT), kHistDevSmem, st, rgb, B, H, W, hs, hg, done);
+  return launch_pdl(k_hist<SW, VEC, NT>, dim3(grid), dim3(NT), kHistDevSmem, st, rgb, B, H, W, hs, hg, done,
+                    (int)nowait);
 }
 
 template <int SW, int VEC>
 cudaError_t launch_nt(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hs, uint32_t* hg, int grid,
-                      int nt, uint32_t* done, cudaStream_t st) {
-  return nt == 256 ? launch_v<SW, VEC, 256>(rgb, B, H, W, hs, hg, grid, done, st)
-                   : launch_v<SW, VEC, kHistThreads>(rgb, B, H, W, hs, hg, grid, done, st);
+                      int nt, uint32_t* done, cudaStream_t st, bool nowait) {
+  return nt == 256 ? launch_v<SW, VEC, 256>(rgb, B, H, W, hs, hg, grid, done, st, nowait)
+                   : launch_v<SW, VEC, kHistThreads>(rgb, B, H, W, hs, hg, grid, done, st, nowait);
 }
 
 bool hist_w8_strip16() {  // measurement switch: HR_HIST_W8=8 keeps the 8-px strips
@@ -414,6 +415,14 @@ bool hist_w8_strip16() {  // measurement switch: HR_HIST_W8=8 keeps the 8-px str
     return e ? atoi(e) : 16;
   }();
   return v != 8;
+}
+
+bool hist_mixed() {  // measurement switch: HR_HIST_MIXED=0 keeps six 8-B loads per strip row
+  static const int v = [] {
+    const char* e = getenv("HR_HIST_MIXED");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
 }
 
 __global__ void __launch_bounds__(256) k_zero(uint4* __restrict__ p, size_t n16) {
@@ -456,9 +465,10 @@ int hist_grid_clamped(int64_t B, int32_t H, int grid) {
 }
 
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
-                        uint32_t* hist_graw, int grid, cudaStream_t st, int nt, uint32_t* done, int tma) {
+                        uint32_t* hist_graw, int grid, cudaStream_t st, int nt, uint32_t* done, int tma,
+                        bool nowait) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(rgb);
-  if (tma && tma_hist_supported(rgb, B, H, W)) {
+  if (tma && !nowait && tma_hist_supported(rgb, B, H, W)) {
     // TMA-staged kernel: one CTA per SM (grid is given for 2 CTAs per SM)
     const int g1 = hist_grid_clamped(B, H, std::max(1, grid / 2));
     if (done) {  // overlapped with the solver: 512 threads, <= 64 registers, image waves
@@ -470,12 +480,13 @@ cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uin
                                                : launch_tma<8>(rgb, B, H, W, hist_s, hist_graw, g1, st);
   }
   grid = hist_grid_clamped(B, H, grid);
-  if (a % 16 == 0 && W % 16 == 0) return launch_nt<16, 16>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st);
+  if (a % 16 == 0 && W % 16 == 0) return launch_nt<16, 16>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait);
   // 8-B aligned rows: 16-px strips of six 8-B loads (the W % 16 == 8 remainder is the scalar tail)
   if (a % 8 == 0 && W % 8 == 0 && W >= 16 && hist_w8_strip16())
-    return launch_nt<16, 8>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st);
-  if (a % 8 == 0 && W % 8 == 0) return launch_nt<8, 8>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st);
-  return launch_nt<16, 1>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st);
+    return hist_mixed() ? launch_nt<16, 9>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait)
+                        : launch_nt<16, 8>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait);
+  if (a % 8 == 0 && W % 8 == 0) return launch_nt<8, 8>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait);
+  return launch_nt<16, 1>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait);
 }
 
 }  // namespace hr

@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
       if (args.queue) st_release(args.queue + atomicAdd(args.queue_tail, 1u), (uint32_t)blockIdx.x + 1u);
     }
   }
-  TRACE_END(3u, (uint32_t)blockIdx.x, tr_mid);
+  TRACE_END(3u, (uint32_t)((uintptr_t)args.hist_s >> 8), tr_mid);  // aux: which launch (group)
 }
 
 // index_1(i, j) of Eqs. 17-19 for every (i, j), once per gamma (R4, R5):

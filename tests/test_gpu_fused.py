@@ -150,23 +150,28 @@ def test_enhance_host_rejects_bad_args():
         m.hr_enhance_host(torch.zeros((2, 4, 4, 3), dtype=torch.uint8, device="cuda"))
 
 
-@pytest.mark.parametrize("knob", ["apply_dyn", "apply_dyn=2", "hist_overlap"])
+@pytest.mark.parametrize("knob", ["apply_dyn", "apply_dyn=2", "apply_dyn=3", "hist_overlap", "groups=2", "groups=3",
+                                  "groups=7", "groups=2,group_apply=0", "groups=3,apply_gs=1"])
 @pytest.mark.parametrize("shape", [(2, 4, 4), (3, 37, 112), (4, 30, 24), (40, 16, 32), (300, 8, 16), (2, 37, 101),
                                    (2, 37, 264), (20, 45, 256), (5, 120, 600), (1, 300, 1920), (150, 16, 256)])
 def test_policy_options_bit_exact(knob, shape):
-    """The optional separate-kernel schedules (completion-order apply from the solver's queue;
-    solvers starting per image during the histogram pass) change only the schedule.  The last
+    """The optional schedules (completion-order or flag-gated ticketed apply; solvers starting per
+    image during the histogram pass; the grouped step, histograms of one group beside the solves
+    of the previous one) change only the schedule.  The last
     five shapes take the TMA histogram kernel in image waves under hist_overlap (W % 16 == 8 with
     odd H; several waves; one image; more images than SMs)."""
     m = hr()
     x = torch.from_numpy(batch(*shape, seed0=17)).cuda()
     ref = [t.cpu() for t in m.hr_enhance_debug(x)]
-    knob, _, val = knob.partition("=")
-    m.set_policy(knob, int(val or 1))
+    kv = [(k, int(v or 1)) for k, _, v in (item.partition("=") for item in knob.split(","))]
+    saved = [(k, m.get_policy(k)) for k, _ in kv]
+    for k, v in kv:
+        m.set_policy(k, v)
     try:
         got = [t.cpu() for t in m.hr_enhance_debug(x)]
         got2 = [t.cpu() for t in m.hr_enhance_debug(x)]  # back-to-back: the queue state resets
     finally:
-        m.set_policy(knob, 0)
+        for k, v in saved:
+            m.set_policy(k, v)
     for a, b, c in zip(ref, got, got2):
         assert torch.equal(a, b) and torch.equal(a, c)

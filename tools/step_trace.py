@@ -53,8 +53,15 @@ def main():
     r = r[r["t0"] >= t_step2 - 1000] if len(hs) else r
     T0 = r["t0"].min()
     print(f"{cfg}: {n} records, step span {(r['t1'].max() - T0) / 1e3:.1f} us  (env: {sys.argv[2:]})")
+    groups = []  # (kind, launch label): histogram / solver launches are told apart by aux
     for k in sorted(set(r["kind"])):
         q = r[r["kind"] == k]
+        if k in (1, 3):
+            for a in sorted(set(q["aux"]), key=lambda a: q[q["aux"] == a]["t0"].min()):
+                groups.append((k, q[q["aux"] == a]))
+        else:
+            groups.append((k, q))
+    for k, q in groups:
         print(f"  {NAMES.get(k, k):11s} CTAs {len(q):4d}  start[us] {pct((q['t0'] - T0) / 1e3)}")
         print(f"  {'':11s}            end[us] {pct((q['t1'] - T0) / 1e3)}")
         if k == 3:
