@@ -48,7 +48,11 @@ constexpr int NW = kSolveWarps;
 //                   runDesc [RR] u32 row order k | lo << 8 | hi << 16 | a << 24, and the
 //                   bin-ordered per-run piece counts / offsets [RR] u32)
 //   s.keyStart[k] = first piece of bin k
-constexpr int kPiece = 8;
+#ifndef HR_KPIECE
+#define HR_KPIECE 8
+#endif
+constexpr int kPiece = HR_KPIECE;
+static_assert(kPiece == 8 || kPiece == 16, "piece length");
 constexpr int kMaxRuns = 32896;                        // sum_{i<256} (i + 1): runs of any image
 constexpr int kMaxPieces = kMaxRuns + 65536 / kPiece;  // P <= RR + E / kPiece
 constexpr int kMaskBytes = kLevels * 8 * 4;            // per-bin row bitmask (8 words per bin)
@@ -399,25 +403,38 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
 
 // sum of h[lo..hi] (hi - lo < kPiece): all loads predicated and in flight at once, fixed tree
 __device__ __forceinline__ double piece_sum(const double* __restrict__ h, int lo, int hi) {
-  static_assert(kPiece == 8, "tree below is for 8 cells");
   const int n = hi - lo;
-  double x[8];
+  double x[kPiece];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) x[m] = (m <= n) ? h[lo + m] : 0.0;
-  return ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
+  for (int m = 0; m < kPiece; ++m) x[m] = (m <= n) ? h[lo + m] : 0.0;
+#pragma unroll
+  for (int w = 1; w < kPiece; w <<= 1)  // pairwise tree: ((x0 + x1) + (x2 + x3)) + ...
+#pragma unroll
+    for (int m = 0; m + w < kPiece; m += 2 * w) x[m] += x[m + w];
+  return x[0];
 }
 
 // sum over bin k of its pieces (contiguous, bin order: runs in row order)
+// (eight accumulators, eight loads in flight per step: the longest bin's chain -- bin 0 of a
+// dark image holds ~60 pieces -- sets the phase time)
 __device__ __forceinline__ double bin_sum(const Sm& s, const RunArena& A, int k) {
-  double e0 = 0.0, e1 = 0.0;
+  double e[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) e[m] = 0.0;
   int j = s.keyStart[k];
   const int j1 = s.keyStart[k + 1];
-  for (; j + 1 < j1; j += 2) {
-    e0 += A.pVal[j];
-    e1 += A.pVal[j + 1];
+  const double* __restrict__ pv = A.pVal;
+  for (; j + 7 < j1; j += 8) {
+    double x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) x[m] = pv[j + m];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) e[m] += x[m];
   }
-  if (j < j1) e0 += A.pVal[j];
-  return e0 + e1;
+#pragma unroll
+  for (int m = 0; m < 7; ++m)
+    if (j + m < j1) e[m] += pv[j + m];
+  return ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
 }
 
 // fast fp64 reciprocal: MUFU.RCP64H seed and two Newton steps (within ~1 ulp)
@@ -468,6 +485,10 @@ __device__ double objective(Sm& s, const hr_params& P, int nR, int nL, double N,
 //   E2  one thread per bin: EstRaw_k over the bin's runs in row order, rho_k (Eq. 11 folded)
 //   R   TPR threads per row: A_a over the row's cells (cached keys kc), Eq. 13
 //   L   TPC threads per column: B_c over the rows, Eq. 12 with the frozen K
+// kTrace: the Eq. 10 objective trace (hr_solve_trace) is compiled into a separate instance, so
+// the product loop stays small (its body must stay resident in the instruction caches: one CTA
+// per image repeats it T times)
+template <bool kTrace>
 __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL, double N, const uint8_t* kc,
                                        const RunArena& A, double* trace = nullptr, int trace_cap = 0) {
   const int tid = threadIdx.x;
@@ -481,7 +502,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
   double QL1 = 0.0;          // sum of the raw hL iterate squared (from the L phase, t > 0)
   int t = 0;
 #ifdef HR_SOLVE_PROFILE
-  long long pacc[6] = {0, 0, 0, 0, 0, 0}, pt0 = clock64(), pt1;
+  long long pacc[16] = {0}, pt0 = clock64(), pt1;
 #define PHASE(i) do { pt1 = clock64(); pacc[i] += pt1 - pt0; pt0 = pt1; } while (0)
 #else
 #define PHASE(i) do { } while (0)
@@ -506,6 +527,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         s.hL2[tid] = n * n;
         q = n * n;
       }
+      PHASE(7);
       {  // piece sums hR_a * sum(hL over the piece); two pieces per step so that their loads
          // are in flight together (restrict: the stores to pVal cannot alias the loads)
         const uint32_t* __restrict__ pd = A.pDesc;
@@ -525,8 +547,10 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
           pv[p] = hr1[d >> 16] * piece_sum(hl1, d & 255, (d >> 8) & 255) * cRL;
         }
       }
+      PHASE(8);
       if (t == 0 || P.use_epsilon) slot_put3(s, R_DR, dr, R_DL, dl, R_SL2, q);
     }
+    PHASE(9);
     __syncthreads();
     PHASE(0);
     if (t > 0) {  // stop rule (R11) on the renormalised iterates of update t
@@ -534,6 +558,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       const bool conv = P.use_epsilon && slot_sum(s, R_DR) <= eps && slot_sum(s, R_DL) <= eps;
       if (conv || t >= P.max_iter) break;
     }
+    PHASE(14);
     // ======== E2: EstRaw_k over the bin's runs (row order) and their pieces; rho_k (Eq. 11) ========
     {
       const int k = tid;
@@ -542,10 +567,12 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         s.rho[k] = form == 0 ? (e > 0.0 ? s.hSd[k] * rcp_fast(e) : 0.0) : s.hSd[k] * e;
       }
     }
+    PHASE(15);
     const double invDenR = rcp_fast((t == 0 ? slot_sum(s, R_SL2) : cL * cL * QL1) * invN2 + P.beta);
+    PHASE(10);
     __syncthreads();
     PHASE(1);
-    if (trace) {  // before Eq. 13
+    if (kTrace) {  // before Eq. 13
       const double F = objective(s, P, nR, nL, N, kc, s.hR, s.hL);
       if (tid == 0 && 3 * t < trace_cap) trace[3 * t] = F;
     }
@@ -556,12 +583,20 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       if (a < nR) {
         const uint8_t* kr = kc + a * nL;
         int c = p;
-        if (form == 0) {
-          for (; c + TPR < nL; c += 2 * TPR) {
-            A0 = fma(s.hL2[c], s.rho[kr[c]], A0);
-            A1 = fma(s.hL2[c + TPR], s.rho[kr[c + TPR]], A1);
+        if (form == 0) {  // four cells per step: keys, then rho and hL^2, all in flight
+          double A2 = 0.0, A3 = 0.0;
+          for (; c + 3 * TPR < nL; c += 4 * TPR) {
+            const int k0 = kr[c], k1 = kr[c + TPR], k2 = kr[c + 2 * TPR], k3 = kr[c + 3 * TPR];
+            A0 = fma(s.hL2[c], s.rho[k0], A0);
+            A1 = fma(s.hL2[c + TPR], s.rho[k1], A1);
+            A2 = fma(s.hL2[c + 2 * TPR], s.rho[k2], A2);
+            A3 = fma(s.hL2[c + 3 * TPR], s.rho[k3], A3);
           }
           if (c < nL) A0 = fma(s.hL2[c], s.rho[kr[c]], A0);
+          if (c + TPR < nL) A1 = fma(s.hL2[c + TPR], s.rho[kr[c + TPR]], A1);
+          if (c + 2 * TPR < nL) A2 = fma(s.hL2[c + 2 * TPR], s.rho[kr[c + 2 * TPR]], A2);
+          A0 += A2;
+          A1 += A3;
         } else {
           for (; c + TPR < nL; c += 2 * TPR) {
             A0 += s.rho[kr[c]];
@@ -570,6 +605,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
           if (c < nL) A0 += s.rho[kr[c]];
         }
       }
+      PHASE(4);
       double A = A0 + A1;
       for (int d = TPR >> 1; d >= 1; d >>= 1) A += __shfl_xor_sync(0xffffffffu, A, d);
       double v = 0.0;
@@ -581,11 +617,13 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         s.hR1[a] = v;
         s.wgt[a] = form == 0 ? v * hr : v * rcp_fast(hr);
       }
+      PHASE(5);
       slot_put3(s, R_SR1, v, R_SR2, v * v, -1, 0.0);
     }
+    PHASE(6);
     __syncthreads();
     PHASE(2);
-    if (trace) {  // after Eq. 13 (raw hR', current hL)
+    if (kTrace) {  // after Eq. 13 (raw hR', current hL)
       const double F = objective(s, P, nR, nL, N, kc, s.hR1, s.hL);
       if (tid == 0 && 3 * t + 1 < trace_cap) trace[3 * t + 1] = F;
     }
@@ -597,12 +635,21 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       if (c < nL) {
         const uint8_t* kq = kc + c;
         int a = p;
-        for (; a + TPC < nR; a += 2 * TPC) {
-          B0 = fma(s.wgt[a], s.rho[kq[a * nL]], B0);
-          B1 = fma(s.wgt[a + TPC], s.rho[kq[(a + TPC) * nL]], B1);
+        double B2 = 0.0, B3 = 0.0;
+        for (; a + 3 * TPC < nR; a += 4 * TPC) {  // four cells per step, keys first
+          const int k0 = kq[a * nL], k1 = kq[(a + TPC) * nL], k2 = kq[(a + 2 * TPC) * nL], k3 = kq[(a + 3 * TPC) * nL];
+          B0 = fma(s.wgt[a], s.rho[k0], B0);
+          B1 = fma(s.wgt[a + TPC], s.rho[k1], B1);
+          B2 = fma(s.wgt[a + 2 * TPC], s.rho[k2], B2);
+          B3 = fma(s.wgt[a + 3 * TPC], s.rho[k3], B3);
         }
         if (a < nR) B0 = fma(s.wgt[a], s.rho[kq[a * nL]], B0);
+        if (a + TPC < nR) B1 = fma(s.wgt[a + TPC], s.rho[kq[(a + TPC) * nL]], B1);
+        if (a + 2 * TPC < nR) B2 = fma(s.wgt[a + 2 * TPC], s.rho[kq[(a + 2 * TPC) * nL]], B2);
+        B0 += B2;
+        B1 += B3;
       }
+      PHASE(11);
       double Bv = B0 + B1;
       for (int d = TPC >> 1; d >= 1; d >>= 1) Bv += __shfl_xor_sync(0xffffffffu, Bv, d);
       double u = 0.0;
@@ -613,11 +660,13 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         u = u > 0.0 ? u : 0.0;
         s.hL1[c] = u;
       }
+      PHASE(12);
       slot_put3(s, R_SL1, u, R_QL1, u * u, -1, 0.0);
     }
+    PHASE(13);
     __syncthreads();
     PHASE(3);
-    if (trace) {  // after Eq. 12 (raw hR', raw hL')
+    if (kTrace) {  // after Eq. 12 (raw hR', raw hL')
       const double F = objective(s, P, nR, nL, N, kc, s.hR1, s.hL1);
       if (tid == 0 && 3 * t + 2 < trace_cap) trace[3 * t + 2] = F;
     }
@@ -628,7 +677,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
   }
 #ifdef HR_SOLVE_PROFILE
   if (blockIdx.x == kProfBlock && threadIdx.x == 0)
-    for (int i = 0; i < 6; ++i) g_solve_clk[512 + i] = pacc[i];
+    for (int i = 0; i < 16; ++i) g_solve_clk[512 + i] = pacc[i];
 #endif
 #undef PHASE
   return t;
@@ -725,7 +774,8 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   PROF_MARK();
 
   double* tr = args.trace ? args.trace + b * (int64_t)args.trace_stride : nullptr;
-  const int t = iterate(s, P, nR, nL, N, kc, A, tr, args.trace_stride);
+  const int t = tr ? iterate<true>(s, P, nR, nL, N, kc, A, tr, args.trace_stride)
+                  : iterate<false>(s, P, nR, nL, N, kc, A, nullptr, 0);
   if (tr && tid == 0)
     for (int i = 3 * t; i < args.trace_stride; ++i) tr[i] = 0.0;
   PROF_MARK();

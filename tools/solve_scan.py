@@ -4,6 +4,7 @@ Each image is solved alone (one CTA) with the phase clocks on; prints the latenc
 distribution and the slowest images with their support sizes and phase split.  The batch's
 solve stage is gated by its slowest image.  Not product code."""
 import ctypes
+import os
 import sys
 
 import numpy as np
@@ -13,7 +14,7 @@ sys.path.insert(0, ".")
 import synth  # noqa: E402
 from paper_2510_21100_b200 import _lib  # noqa: E402
 
-lib = ctypes.CDLL("tools/libhistretinex_prof.so")
+lib = ctypes.CDLL(os.environ.get("HR_PROF_LIB", "tools/libhistretinex_prof.so"))
 vp = ctypes.c_void_p
 ctx = vp()
 assert lib.hr_create(ctypes.byref(ctx), 0) == 0
@@ -52,7 +53,7 @@ for cfg, nimg in (("C3", 64), ("C5", 64), ("C2", 1), ("C4", 1)):
         sl = [int(v) for v in full[600:621]]
         rb1 = [sl[i + 1] - sl[i] for i in range(6)]
         rb2 = [sl[11 + i] - sl[10 + i] for i in range(6)]
-        rows.append((int(c[-1] - c[0]), b, nL, nR, d.tolist(), [int(v) for v in full[512:516]], int(it.item()),
+        rows.append((int(c[-1] - c[0]), b, nL, nR, d.tolist(), [int(v) for v in full[512:528]], int(it.item()),
                      rb1, rb2))
     tot = np.array([r[0] for r in rows]) / GHZ / 1e3
     print(f"== {cfg}: {B} images, solve latency us: min {tot.min():.1f} p50 {np.median(tot):.1f} "
@@ -60,6 +61,10 @@ for cfg, nimg in (("C3", 64), ("C5", 64), ("C2", 1), ("C4", 1)):
     for r in sorted(rows, reverse=True)[:6]:
         print(f"   img {r[1]:3d} nL={r[2]:3d} nR={r[3]:3d} E={r[2] * r[3]:5d} iters={r[6]:2d} "
               f"total {r[0] / GHZ / 1e3:6.1f} us  [hist,supp,runs,iters,eq20]={r[4]}  per-iter [E1,E2,R,L]="
-              f"{[round(v / max(r[6], 1)) for v in r[5]]}")
+              f"{[round(v / max(r[6], 1)) for v in r[5][:4]]}")
+        print("      sub-phases per iter: E1[renorm,pieces,slot,bar]=%s E2[stopchk,bins,rcp,bar]=%s R[walk,shfl+v,slot,bar]=%s "
+              "L[walk,shfl+u,slot,bar]=%s" % tuple(
+                  str([round(r[5][i] / max(r[6], 1)) for i in ix]) for ix in ((7, 8, 9, 0), (14, 15, 10, 1), (4, 5, 6, 2),
+                                                                              (11, 12, 13, 3))))
         print(f"      run_build steps [count+scan, desc, fix+mask, keyscan, slots, pieces+scan/write]: {r[7]}"
               f"  eq20 build: {r[8]}")
