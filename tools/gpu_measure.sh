@@ -3,7 +3,7 @@
 #   and full captures of the streaming kernels, per-image solver latencies.
 # Each command runs plain before any ncu pass of it (ncu numbers are never bench values).
 set -x
-bash tools/build_measure_libs.sh >/dev/null 2>&1 || true
+ls tools/*.so >/dev/null 2>&1 || bash tools/build_measure_libs.sh >/dev/null 2>&1 || true
 python -m pytest tests -q -m gpu -rf --timeout 900 -x > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
 HR_LIB=tools/libhistretinex_check.so python -m pytest tests -q -m gpu -x --timeout 900 2>&1 | tail -1
 python -c "import __graft_entry__ as g; g.smoke()"
