@@ -166,6 +166,38 @@ def test_histogram_tma_kernel(shape, tma):
             f"raw gradient histogram {b}"
 
 
+# Direct-load kernel with 8-B aligned rows (W % 8 == 0): 16-px strips with mixed 16-B / 8-B
+# loads by row parity, and for W % 16 == 8 the half-strip walkers (the last 8 columns, in warps
+# of their own; one row group fewer when needed).  Base offset 8 makes every row of a W % 16 == 0
+# image 8 mod 16 (the four-load form) and flips the parity pattern of W % 16 == 8 rows; noise
+# takes the checked gradient path (strong edges) inside the half strips too; W = 24 has one full
+# strip per row, W = 8 none (scalar tail only), W = 8200 more strips than threads.
+HALF_SHAPES = [(2, 37, 24), (3, 5, 8), (2, 33, 40), (1, 41, 600), (5, 23, 120), (2, 9, 1000), (1, 3, 8200),
+               (2, 64, 592), (1, 1, 600), (1, 2, 600)]
+
+
+@pytest.mark.parametrize("shape", HALF_SHAPES)
+@pytest.mark.parametrize("offset", [0, 8])
+@pytest.mark.parametrize("kind", ["img", "noise"])
+def test_histogram_half_strips_and_mixed_loads(shape, offset, kind):
+    B, H, W = shape
+    if kind == "noise":
+        x = np.random.default_rng(H * W + B + offset).integers(0, 256, size=(B, H, W, 3), dtype=np.uint8)
+    else:
+        x = np.stack([synth.make_image(H, W, seed=400 + b, peak=0.05 + 0.2 * b) for b in range(B)])
+    n = x.size
+    buf = torch.zeros(n + 16, dtype=torch.uint8, device="cuda")
+    buf[offset:offset + n] = to_dev(x).reshape(-1)
+    xd = buf[offset:offset + n].view(B, H, W, 3)
+    hs, hg, hgr = hr().hr_histogram(xd)
+    hs, hgr = hs.cpu().numpy(), hgr.cpu().numpy()
+    for b in range(B):
+        S = oracle.value_channel(x[b])
+        assert np.array_equal(hs[b].astype(np.uint64), oracle.count_histogram(S, 256)), f"hist_s {b}"
+        assert np.array_equal(hgr[b, :511].astype(np.uint64), oracle.count_histogram(oracle.gradient_raw(S), 511)), \
+            f"raw gradient histogram {b}"
+
+
 def test_histogram_unaligned_base():
     x = synth.make_image(40, 64, seed=5)
     buf = torch.zeros(40 * 64 * 3 + 1, dtype=torch.uint8, device="cuda")
