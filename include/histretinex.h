@@ -243,6 +243,10 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
                     -1: auto = 2 when 2 <= B <= #SMs / 2, else off
      "group_apply"  grouped step's apply: 0 static shares (groups 0..G-2, then     default 0
                     the last group); 1 the last group by CTA tickets
+     "solve_waves"  separate kernels, B > #SMs: one solver CTA per SM solving    default 0
+                    its images in turn, the apply beside it (off: the solver and
+                    apply CTAs do not share SMs; C5 0.203-0.261 vs 0.175 ms)
+     "solve_waves_ag" apply CTAs per SM launched with solve_waves (1..2)         default 1
      "hist_tma"     histogram kernel with TMA-staged rows (one CTA per SM; in     default 0
                     the hist_overlap form 512 threads in image waves) for 16-B
                     aligned batches with W % 16 == 0 (256 <= W <= 8192) or

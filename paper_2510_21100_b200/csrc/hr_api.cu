@@ -43,6 +43,8 @@ struct hr_ctx {
                           // (off: the 16-warp histogram pass costs more than the overlap saves)
   int group_apply = 0;    // grouped step's apply: 0 = static shares of groups 0..G-2, then of the
                           // last group; 1 = last group by CTA tickets (measured slower)
+  int solve_waves = 0;    // separate kernels, B > SMs: one solver CTA per SM solving images in turn
+  int solve_waves_ag = 1; // ... apply CTAs per SM launched beside it
   int groups = -1;        // grouped step (>= 2): histograms of group k+1 run beside the solves of
                           // group k, the apply beside the last group's solves (0/1: off)
   int64_t launches = 0;   // kernels launched through this context (hr_kernel_launches)
@@ -215,6 +217,8 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_APPLY_DYN")) c->apply_dyn = atoi(v) >= 0 && atoi(v) <= 3 ? atoi(v) : 0;
   if (const char* v = getenv("HR_APPLY_GS")) c->apply_gs = atoi(v) > 0 ? atoi(v) : 8;
   if (const char* v = getenv("HR_GROUP_APPLY")) c->group_apply = atoi(v) != 0;
+  if (const char* v = getenv("HR_SOLVE_WAVES")) c->solve_waves = atoi(v) != 0;
+  if (const char* v = getenv("HR_SOLVE_WAVES_AG")) c->solve_waves_ag = atoi(v) == 2 ? 2 : 1;
   if (const char* v = getenv("HR_GROUPS")) c->groups = atoi(v) >= -1 && atoi(v) <= 64 ? atoi(v) : -1;
   *out = c;
   return HR_OK;
@@ -264,7 +268,8 @@ const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
       {"solve_cpsm", &c->solve_cpsm, 0, 2},         {"hist_overlap", &c->hist_overlap, 0, 1},
       {"apply_dyn", &c->apply_dyn, 0, 3},           {"apply_gs", &c->apply_gs, 1, 1 << 20},
       {"hist_tma", &c->hist_tma, 0, 1},             {"groups", &c->groups, -1, 64},
-      {"group_apply", &c->group_apply, 0, 1},
+      {"group_apply", &c->group_apply, 0, 1},       {"solve_waves", &c->solve_waves, 0, 1},
+      {"solve_waves_ag", &c->solve_waves_ag, 1, 2},
   };
   for (const Knob& k : knobs)
     if (strcmp(k.name, key) == 0) {
@@ -472,7 +477,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   };
   auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, uint32_t* ready = nullptr,
                          const uint32_t* hist_done = nullptr, int hist_bands = 0, uint32_t* queue = nullptr,
-                         uint32_t* queue_tail = nullptr, int cpsm = 0) -> cudaError_t {
+                         uint32_t* queue_tail = nullptr, int cpsm = 0, int max_ctas = 0) -> cudaError_t {
     hr::SolveArgs a{};
     a.ready = c->warp_solver ? nullptr : ready;
     a.queue = c->warp_solver ? nullptr : queue;
@@ -480,6 +485,11 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     a.hist_done = c->warp_solver ? nullptr : hist_done;
     a.hist_H = H;
     a.arena_bytes = hist_done ? kOverlapArena : 0;  // fits beside two histogram CTAs
+    if (max_ctas > 0 && !hist_done) {
+      // one solver CTA per SM beside one apply CTA: too large for two solvers on an SM (113.5 KB
+      // + 1 KB reserved each > 228 KB), small enough for a solver and an apply CTA
+      a.arena_bytes = 116224 - (int)(hr::solve_smem_bytes(1) - 1);
+    }
     a.idx1_tab = tab;
     a.hist_s = hs + b0 * kLevels;
     a.hist_g = nullptr;
@@ -498,7 +508,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       return r;
     }
     a.lut = lut + b0 * kLevels;  // CDF + LUT tail fused into the solver CTA (no target round trip)
-    return counted(c, hr::launch_solve(a, nb, hist_done ? 2 : cpsm ? cpsm : solve_cpsm_for(c, nb), s));
+    return counted(c, hr::launch_solve(a, nb, hist_done ? 2 : cpsm ? cpsm : solve_cpsm_for(c, nb), s, max_ctas));
   };
   auto apply_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, const uint32_t* ready = nullptr) -> cudaError_t {
     return counted(c, hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s,
@@ -636,14 +646,20 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     // completion-order apply: k_solve appends each finished image to a queue in the control block
     const bool dyn = c->apply_dyn && ready && !c->warp_solver && hr::apply_dyn_supported(in, out, B, H, W);
     uint32_t* queue = dyn && c->apply_dyn == 1 ? ctl + hr::kCtlHeader + 2 * B : nullptr;
+    // solve waves (B > #SMs): one solver CTA per SM solving its images in turn (the first wave's
+    // LUTs complete early), the apply at one CTA per SM beside it, every apply CTA taking its share
+    // of the first wave's images first
+    const bool waves = c->solve_waves && ready && !overlap && !dyn && B > c->num_sms;
     if (e == cudaSuccess)
       e = solve_chunk(0, B, st, ready, overlap ? ctl + hr::kCtlHeader : nullptr, overlap ? HG : 0, queue,
-                      queue ? ctl + 2 : nullptr);
+                      queue ? ctl + 2 : nullptr, waves ? 2 : 0, waves ? c->num_sms : 0);
     if (e == cudaSuccess) e = mark(2);
     if (e == cudaSuccess)
       e = dyn ? counted(c, hr::launch_apply_dyn(in, lut, B, H, W, out, apply_grid(c), queue, ctl + 3, c->apply_gs, st,
                                                 c->apply_dyn == 3 ? ready : nullptr, c->apply_dyn == 3 ? B / 2 : 0))
-              : apply_chunk(0, B, st, ready);
+              : waves ? counted(c, hr::launch_apply(in, lut, B, H, W, out, c->solve_waves_ag * c->num_sms, st, ready,
+                                                    c->num_sms))
+                      : apply_chunk(0, B, st, ready);
     if (e == cudaSuccess) e = mark(3);
     return cuda_err(c, e, "hr_enhance");
   }

@@ -193,11 +193,15 @@ struct SolveArgs {
   int32_t arena_bytes;           // shared run arena per CTA (0: the default 80 KB)
   double* trace;                 // [B][trace_stride] nullable: Eq. 10 objective, 3 values per update
   int32_t trace_stride;
+  int64_t nimg;                  // > 0: images solved by a grid of fewer CTAs (CTA c: c, c + grid, ...);
+                                 // 0: one image per CTA
 };
 // warp-per-image solver for nR <= 32; flags the other images in deferred[b] (then run k_solve)
 cudaError_t launch_solve_warp(const SolveArgs& a, int64_t B, int32_t* deferred, cudaStream_t st);
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st);
-cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t st);
+// max_ctas > 0: at most that many CTAs, each solving images c, c + grid, ... in turn (releasing
+// each image's ready flag as it completes)
+cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t st, int max_ctas = 0);
 size_t solve_smem_bytes(int arena_bytes = 0);
 size_t solve_cells_ws_bytes(int64_t B);
 

@@ -16,29 +16,36 @@ __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
   TRACE_T0();
   unsigned long long tr_mid = 0ull;
   (void)tr_mid;
-  if (args.hist_done) {  // overlap the histogram pass: wait for this image's rows only
-    pdl_trigger();
-    if (threadIdx.x == 0) {
-      const uint32_t need = (uint32_t)args.hist_H;
-      long long spins = 0;
-      while (ld_acquire(args.hist_done + blockIdx.x) < need) {
-        __nanosleep(256);
-        if (++spins > (1LL << 25)) asm volatile("trap;");  // ~10 s: a logic error, not a wait
-      }
-    }
-    __syncthreads();
-  } else {
+  if (!args.hist_done) {
     pdl_wait();
     pdl_trigger();
+  } else {
+    pdl_trigger();
   }
-  TRACE_MID(tr_mid);
-  solve_image(args, blockIdx.x, smraw, wscr);
-  if (args.ready || args.queue) {  // every exit of solve_image arrives here: LUT written
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (args.ready) st_release(args.ready + blockIdx.x, 1u);
-      if (args.queue) st_release(args.queue + atomicAdd(args.queue_tail, 1u), (uint32_t)blockIdx.x + 1u);
+  // one image per CTA, or (nimg > 0) images blockIdx.x, blockIdx.x + gridDim.x, ... in turn
+  const int64_t n = args.nimg > 0 ? args.nimg : (int64_t)gridDim.x;
+  for (int64_t b = blockIdx.x; b < n; b += gridDim.x) {
+    if (args.hist_done) {  // overlap the histogram pass: wait for this image's rows only
+      if (threadIdx.x == 0) {
+        const uint32_t need = (uint32_t)args.hist_H;
+        long long spins = 0;
+        while (ld_acquire(args.hist_done + b) < need) {
+          __nanosleep(256);
+          if (++spins > (1LL << 25)) asm volatile("trap;");  // ~10 s: a logic error, not a wait
+        }
+      }
+      __syncthreads();
+    }
+    TRACE_MID(tr_mid);
+    solve_image(args, b, smraw, wscr);
+    __syncthreads();  // every exit of solve_image arrives here: LUT written, shared state free
+    if (args.ready || args.queue) {
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (args.ready) st_release(args.ready + b, 1u);
+        if (args.queue) st_release(args.queue + atomicAdd(args.queue_tail, 1u), (uint32_t)b + 1u);
+      }
     }
   }
   TRACE_END(3u, (uint32_t)((uintptr_t)args.hist_s >> 8), tr_mid);  // aux: which launch (group)
@@ -93,7 +100,7 @@ size_t solve_cells_ws_bytes(int64_t B) { return (size_t)B * (size_t)kArenaGlobal
 // solves onto one SM while others idle).  The shared memory that placement reserves anyway is
 // given to the run arena (kBigArena), so images with large supports (C4: E = 8480 cells) keep
 // their run structure in shared memory instead of the global arena.
-cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t st) {
+cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t st, int max_ctas) {
   constexpr int kBigArena = 190 * 1024;  // sizeof(Sm) + 190 KB <= 227 KB per block
   static bool attr = false;
   if (!attr) {
@@ -106,7 +113,9 @@ cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t 
   }
   SolveArgs a = a0;
   if (cpsm == 1 && a.arena_bytes == 0) a.arena_bytes = kBigArena;
-  return launch_pdl(k_solve, dim3((unsigned)B), dim3(T), solve_smem_bytes(a.arena_bytes), st, a);
+  const int64_t grid = max_ctas > 0 ? std::min<int64_t>(B, max_ctas) : B;
+  a.nimg = grid < B ? B : 0;  // fewer CTAs than images: each CTA solves several in turn
+  return launch_pdl(k_solve, dim3((unsigned)grid), dim3(T), solve_smem_bytes(a.arena_bytes), st, a);
 }
 
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st) {
