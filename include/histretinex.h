@@ -243,6 +243,10 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
                     -1: auto = 2 when 2 <= B <= #SMs / 2, else off
      "group_apply"  grouped step's apply: 0 static shares (groups 0..G-2, then     default 0
                     the last group); 1 the last group by CTA tickets
+     "solve_wide_px" hr_enhance, one solver CTA per SM (B <= #SMs): 512-thread   default 4194304
+                    solver CTAs for images of H*W >= value pixels (0: never; large
+                    images have large supports: C4 103 vs 121 us per image, while
+                    small supports are faster at 256 threads: C2 37 vs 43 us)
      "solve_waves"  separate kernels, B > #SMs: one solver CTA per SM solving    default 0
                     its images in turn, the apply beside it (off: the solver and
                     apply CTAs do not share SMs; C5 0.203-0.261 vs 0.175 ms)

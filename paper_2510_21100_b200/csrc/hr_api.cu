@@ -43,6 +43,7 @@ struct hr_ctx {
                           // (off: the 16-warp histogram pass costs more than the overlap saves)
   int group_apply = 0;    // grouped step's apply: 0 = static shares of groups 0..G-2, then of the
                           // last group; 1 = last group by CTA tickets (measured slower)
+  int solve_wide_px = 4 << 20;  // hr_enhance: 512-thread solver CTAs (one per SM) for H*W >= this (0: never)
   int solve_waves = 0;    // separate kernels, B > SMs: one solver CTA per SM solving images in turn
   int solve_waves_ag = 1; // ... apply CTAs per SM launched beside it
   int groups = -1;        // grouped step (>= 2): histograms of group k+1 run beside the solves of
@@ -218,6 +219,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_APPLY_GS")) c->apply_gs = atoi(v) > 0 ? atoi(v) : 8;
   if (const char* v = getenv("HR_GROUP_APPLY")) c->group_apply = atoi(v) != 0;
   if (const char* v = getenv("HR_SOLVE_WAVES")) c->solve_waves = atoi(v) != 0;
+  if (const char* v = getenv("HR_SOLVE_WIDE_PX")) c->solve_wide_px = atoi(v) >= 0 ? atoi(v) : 4 << 20;
   if (const char* v = getenv("HR_SOLVE_WAVES_AG")) c->solve_waves_ag = atoi(v) == 2 ? 2 : 1;
   if (const char* v = getenv("HR_GROUPS")) c->groups = atoi(v) >= -1 && atoi(v) <= 64 ? atoi(v) : -1;
   *out = c;
@@ -269,7 +271,7 @@ const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
       {"apply_dyn", &c->apply_dyn, 0, 3},           {"apply_gs", &c->apply_gs, 1, 1 << 20},
       {"hist_tma", &c->hist_tma, 0, 1},             {"groups", &c->groups, -1, 64},
       {"group_apply", &c->group_apply, 0, 1},       {"solve_waves", &c->solve_waves, 0, 1},
-      {"solve_waves_ag", &c->solve_waves_ag, 1, 2},
+      {"solve_waves_ag", &c->solve_waves_ag, 1, 2}, {"solve_wide_px", &c->solve_wide_px, 0, 1 << 30},
   };
   for (const Knob& k : knobs)
     if (strcmp(k.name, key) == 0) {
@@ -508,7 +510,10 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       return r;
     }
     a.lut = lut + b0 * kLevels;  // CDF + LUT tail fused into the solver CTA (no target round trip)
-    return counted(c, hr::launch_solve(a, nb, hist_done ? 2 : cpsm ? cpsm : solve_cpsm_for(c, nb), s, max_ctas));
+    // 512-thread solver CTAs for large images (their supports, and so the cell loops, tend to be
+    // large: C4 33 MP 8,480 cells; C2 0.66 MP 1,334 cells)
+    const bool wide = c->solve_wide_px > 0 && (int64_t)H * W >= c->solve_wide_px;
+    return counted(c, hr::launch_solve(a, nb, hist_done ? 2 : cpsm ? cpsm : solve_cpsm_for(c, nb), s, max_ctas, wide));
   };
   auto apply_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, const uint32_t* ready = nullptr) -> cudaError_t {
     return counted(c, hr::launch_apply(in + b0 * img, lut + b0 * kLevels, nb, H, W, out + b0 * img, apply_grid(c), s,

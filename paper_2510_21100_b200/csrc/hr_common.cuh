@@ -201,7 +201,10 @@ cudaError_t launch_solve_warp(const SolveArgs& a, int64_t B, int32_t* deferred, 
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st);
 // max_ctas > 0: at most that many CTAs, each solving images c, c + grid, ... in turn (releasing
 // each image's ready flag as it completes)
-cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t st, int max_ctas = 0);
+// wide (with cpsm == 1): 512-thread CTAs (large supports: C4 103 vs 121 us per image; small ones
+// are faster at 256 threads: C2 37 vs 43 us)
+cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t st, int max_ctas = 0,
+                         bool wide = false);
 size_t solve_smem_bytes(int arena_bytes = 0);
 size_t solve_cells_ws_bytes(int64_t B);
 

@@ -71,7 +71,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 template <int SW, int VEC>
 __global__ void __launch_bounds__(kFT, 2) k_fused(const FusedArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ int wscr[NW];
+  __shared__ int wscr[kFT / 32];
   __shared__ uint32_t meta[kWarps][kStages];
   __shared__ int sh;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kFT, 2) k_fused(const FusedArgs a) {
       TRACE_T(ts0);
 #endif
       __threadfence();
-      solve_image(a.sa, b, smraw, wscr);
+      solve_image<kFT>(a.sa, b, smraw, wscr);
       __threadfence();
       __syncthreads();
       if (tid == 0) st_release(ready + b, 1u);

@@ -4,15 +4,18 @@
 // Standalone launches of the solver (one CTA per image), the per-gamma index_1 table, the
 // gradient remap and the CDF/LUT match.  The device body is in solve_dev.cuh.
 #include <algorithm>
+#include <cstdlib>
 
 #include "solve_dev.cuh"
 
 namespace hr {
 namespace {
 
-__global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
+// NT = 256: two CTAs per SM (batches); NT = 512: one CTA per SM, the cell loops over 16 warps
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_solve(SolveArgs args) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ int wscr[NW];
+  __shared__ int wscr[NT / 32];
   TRACE_T0();
   unsigned long long tr_mid = 0ull;
   (void)tr_mid;
@@ -37,7 +40,7 @@ __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
       __syncthreads();
     }
     TRACE_MID(tr_mid);
-    solve_image(args, b, smraw, wscr);
+    solve_image<NT>(args, b, smraw, wscr);
     __syncthreads();  // every exit of solve_image arrives here: LUT written, shared state free
     if (args.ready || args.queue) {
       __threadfence();
@@ -53,7 +56,7 @@ __global__ void __launch_bounds__(T, 2) k_solve(SolveArgs args) {
 
 // index_1(i, j) of Eqs. 17-19 for every (i, j), once per gamma (R4, R5):
 // p_j = b_j^(1/gamma) (b_j itself when gamma == 1), first k minimising |b_i p_j - b_k|.
-__global__ void __launch_bounds__(T) k_idx1_table(double gamma, uint8_t* tab) {
+__global__ void __launch_bounds__(kLevels) k_idx1_table(double gamma, uint8_t* tab) {
   __shared__ double bk[kLevels], pj[kLevels];
   const int j = threadIdx.x;
   bk[j] = (double)j / 255.0;
@@ -63,24 +66,24 @@ __global__ void __launch_bounds__(T) k_idx1_table(double gamma, uint8_t* tab) {
   tab[i * kLevels + j] = (uint8_t)idx1(bk, bk[i], pj[j]);
 }
 
-__global__ void __launch_bounds__(T) k_remap(const uint32_t* graw, int32_t grad_norm, uint32_t* hist_g) {
+__global__ void __launch_bounds__(kLevels) k_remap(const uint32_t* graw, int32_t grad_norm, uint32_t* hist_g) {
   __shared__ uint32_t h[kLevels];
-  __shared__ int wscr[NW];
+  __shared__ int wscr[kLevels / 32];
   const int64_t b = blockIdx.x;
-  remap_gradient(graw + b * kGradSlots, grad_norm, h, wscr);
+  remap_gradient<kLevels>(graw + b * kGradSlots, grad_norm, h, wscr);
   hist_g[b * kLevels + threadIdx.x] = h[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(T) k_match(const uint32_t* hist_s, const double* target, uint8_t* lut,
+__global__ void __launch_bounds__(kLevels) k_match(const uint32_t* hist_s, const double* target, uint8_t* lut,
                                              int32_t* status) {
   __shared__ uint32_t hSi[kLevels];
   __shared__ double Tt[kLevels], Pt[kLevels], Ct[kLevels], Cs[kLevels];
-  __shared__ int wscr[NW];
+  __shared__ int wscr[kLevels / 32];
   const int64_t b = blockIdx.x;
   hSi[threadIdx.x] = hist_s[b * kLevels + threadIdx.x];
   Tt[threadIdx.x] = target[b * kLevels + threadIdx.x];
   __syncthreads();
-  cdf_lut(hSi, Tt, Pt, Ct, Cs, wscr, lut + b * kLevels, status ? status + b : nullptr);
+  cdf_lut<kLevels>(hSi, Tt, Pt, Ct, Cs, wscr, lut + b * kLevels, status ? status + b : nullptr);
 }
 
 }  // namespace
@@ -100,14 +103,17 @@ size_t solve_cells_ws_bytes(int64_t B) { return (size_t)B * (size_t)kArenaGlobal
 // solves onto one SM while others idle).  The shared memory that placement reserves anyway is
 // given to the run arena (kBigArena), so images with large supports (C4: E = 8480 cells) keep
 // their run structure in shared memory instead of the global arena.
-cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t st, int max_ctas) {
+cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t st, int max_ctas, bool wide) {
   constexpr int kBigArena = 190 * 1024;  // sizeof(Sm) + 190 KB <= 227 KB per block
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)solve_smem_bytes(kBigArena));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_solve, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    cudaError_t e = cudaSuccess;
+    for (auto k : {k_solve<256>, k_solve<512>}) {
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem_bytes(kBigArena));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    }
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -115,23 +121,25 @@ cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t 
   if (cpsm == 1 && a.arena_bytes == 0) a.arena_bytes = kBigArena;
   const int64_t grid = max_ctas > 0 ? std::min<int64_t>(B, max_ctas) : B;
   a.nimg = grid < B ? B : 0;  // fewer CTAs than images: each CTA solves several in turn
-  return launch_pdl(k_solve, dim3((unsigned)grid), dim3(T), solve_smem_bytes(a.arena_bytes), st, a);
+  if (cpsm == 1 && wide)
+    return launch_pdl(k_solve<512>, dim3((unsigned)grid), dim3(512), solve_smem_bytes(a.arena_bytes), st, a);
+  return launch_pdl(k_solve<256>, dim3((unsigned)grid), dim3(256), solve_smem_bytes(a.arena_bytes), st, a);
 }
 
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st) {
-  k_idx1_table<<<kLevels, T, 0, st>>>(gamma, tab);
+  k_idx1_table<<<kLevels, kLevels, 0, st>>>(gamma, tab);
   return cudaGetLastError();
 }
 
 cudaError_t launch_remap(const uint32_t* hist_graw, int64_t B, int32_t grad_norm, uint32_t* hist_g,
                          cudaStream_t st) {
-  k_remap<<<(unsigned)B, T, 0, st>>>(hist_graw, grad_norm, hist_g);
+  k_remap<<<(unsigned)B, kLevels, 0, st>>>(hist_graw, grad_norm, hist_g);
   return cudaGetLastError();
 }
 
 cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,
                          int32_t* status, cudaStream_t st) {
-  k_match<<<(unsigned)B, T, 0, st>>>(hist_s, target, lut, status);
+  k_match<<<(unsigned)B, kLevels, 0, st>>>(hist_s, target, lut, status);
   return cudaGetLastError();
 }
 

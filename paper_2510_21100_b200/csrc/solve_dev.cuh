@@ -38,8 +38,10 @@
 namespace hr {
 namespace {
 
-constexpr int T = kSolveThreads;
-constexpr int NW = kSolveWarps;
+// Thread count T of a solver CTA is a template parameter: 256 (batched; 2 CTAs per SM) or 512
+// (few images: one CTA per SM, the cell loops spread over twice the warps).  Bin-indexed steps
+// use threads 0..255 (thread k <-> bin k); the others only join the cell loops and barriers.
+constexpr int kMaxSW = 16;  // warps of the widest solver CTA
 // Run arena (per image): runs = maximal equal-key segments of a compacted row; pieces = runs
 // cut into at most kPiece cells (bounds the per-thread sum chains of the E1 phase).  Pieces
 // are stored in BIN order (bin, then row, then position), so a bin's pieces are contiguous:
@@ -100,11 +102,11 @@ struct __align__(16) Sm {
   double hSd[kLevels];                // dense hS as double
   double rho[kLevels];                // rho_k (GC) or sigma_k (paper-literal)
   double bk[kLevels];                 // b_k = k/255 (R1)
-  double red[kSlots][NW];
+  double red[kSlots][kMaxSW];
   uint32_t hSi[kLevels], hGi[kLevels];
   int keyStart[kLevels + 1];  // piece offsets per bin (bin order)
   uint8_t listR[kLevels], listL[kLevels];
-  unsigned long long nw[NW];
+  unsigned long long nw[kMaxSW];
 };
 
 __device__ __forceinline__ int idx0(int i, int j) {  // P:192 index(i,j) for l = 256
@@ -112,7 +114,9 @@ __device__ __forceinline__ int idx0(int i, int j) {  // P:192 index(i,j) for l =
 }
 
 // Sum over warps in fixed order (call after a barrier that follows the slot writes).
+template <int T>
 __device__ __forceinline__ double slot_sum(const Sm& s, int slot) {
+  constexpr int NW = T / 32;
   double a = 0.0;
 #pragma unroll
   for (int w = 0; w < NW; ++w) a += s.red[slot][w];
@@ -137,7 +141,9 @@ __device__ __forceinline__ void slot_put3(Sm& s, int s0, double v0, int s1, doub
 }
 
 
+template <int T>
 __device__ int block_scan_excl(int x, int* total, int* wscratch) {
+  constexpr int NW = T / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int v = x;
 #pragma unroll
@@ -179,26 +185,29 @@ __device__ __forceinline__ int idx1(const double* bk, double bi, double pj) {
 
 // CDF + LUT (R16), shared by the solver tail and k_match.  T: dense target [256] in
 // smem, hSi: dense counts in smem.  Uses Pt/Ct/Cs scratch (3 x 256 doubles).
+template <int T>
 __device__ void cdf_lut(const uint32_t* hSi, const double* Tt, double* Pt, double* Ct, double* Cs,
                         int* wscr, uint8_t* lut_out, int32_t* status_out) {
+  constexpr int NB = kLevels / 32;  // warps holding bins (thread k <-> bin k)
   const int tid = threadIdx.x, lane = tid & 31;
+  const bool bin = tid < kLevels;
   // integer prefix of hS (exact in any order)
-  unsigned long long v = hSi[tid];
+  unsigned long long v = bin ? hSi[tid] : 0ull;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const unsigned long long u = __shfl_up_sync(0xffffffffu, v, d);
     if (lane >= d) v += u;
   }
-  __shared__ unsigned long long wtot[NW];
-  if (lane == 31) wtot[tid >> 5] = v;
+  __shared__ unsigned long long wtot[NB];
+  if (lane == 31 && bin) wtot[tid >> 5] = v;
   __syncthreads();
   unsigned long long off = 0, Ntot = 0;
-  for (int u = 0; u < NW; ++u) {
+  for (int u = 0; u < NB; ++u) {
     if (u < (tid >> 5)) off += wtot[u];
     Ntot += wtot[u];
   }
   const unsigned long long Ps = off + v;
-  Cs[tid] = Ntot ? (double)Ps / (double)Ntot : 0.0;
+  if (bin) Cs[tid] = Ntot ? (double)Ps / (double)Ntot : 0.0;
   // plateau-preserving prefix of the target: lane-sequential blocks of 8, sequential carry
   if (tid < 32) {
     double loc[8];
@@ -220,10 +229,10 @@ __device__ void cdf_lut(const uint32_t* hSi, const double* Tt, double* Pt, doubl
   __syncthreads();
   const double last = Pt[kLevels - 1];
   const bool degenerate = !(last > 0.0) || Ntot == 0;
-  Ct[tid] = degenerate ? 0.0 : Pt[tid] / last;
+  if (bin) Ct[tid] = degenerate ? 0.0 : Pt[tid] / last;
   __syncthreads();
   int res = tid;
-  if (!degenerate) {
+  if (bin && !degenerate) {
     const double x = Cs[tid];
     // k* = first k with Ct[k] >= x
     int lo = 0, hi = kLevels;
@@ -246,19 +255,23 @@ __device__ void cdf_lut(const uint32_t* hSi, const double* Tt, double* Pt, doubl
       if (d0 <= d1) res = l2;  // ties -> smallest k
     }
   }
-  if (lut_out) lut_out[tid] = (uint8_t)res;
+  if (lut_out && bin) lut_out[tid] = (uint8_t)res;
   if (status_out && tid == 0) *status_out = degenerate ? (int32_t)HR_EDEGENERATE : (int32_t)HR_OK;
   (void)wscr;
 }
 
+template <int T>
 __device__ void remap_gradient(const uint32_t* graw, int grad_norm, uint32_t* hGi, int* wscr) {
+  constexpr int NW = T / 32;
+  static_assert(2 * 256 == kGradSlots && (T == 256 || T == 512), "gradient slots per thread");
   const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t c0 = __ldcg(graw + tid), c1 = __ldcg(graw + tid + T);
-  int m = c1 ? tid + T : (c0 ? tid : 0);
+  // slots tid and tid + 256 (T = 256) or tid (T = 512)
+  const uint32_t c0 = __ldcg(graw + tid), c1 = T == 256 ? __ldcg(graw + tid + 256) : 0u;
+  int m = c1 ? tid + 256 : (c0 ? tid : 0);
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
   if (lane == 0) wscr[tid >> 5] = m;
-  hGi[tid] = 0u;
+  if (tid < kLevels) hGi[tid] = 0u;
   __syncthreads();
   int gmax = 0;
   for (int u = 0; u < NW; ++u) gmax = max(gmax, wscr[u]);
@@ -267,7 +280,7 @@ __device__ void remap_gradient(const uint32_t* graw, int grad_norm, uint32_t* hG
     return gmax == 0 ? 0 : (int)((510u * (uint32_t)g + (uint32_t)gmax) / (2u * (uint32_t)gmax));  // MAXNORM
   };
   if (c0) atomicAdd(&hGi[level(tid)], c0);
-  if (c1) atomicAdd(&hGi[level(tid + T)], c1);
+  if (c1) atomicAdd(&hGi[level(tid + 256)], c1);
   __syncthreads();
 }
 
@@ -295,6 +308,7 @@ struct RunArena {
 // its bin-ordered slot = (runs of smaller bins) + rank of its row among the bin's rows.  A
 // scan of the per-slot piece counts places every piece in bin order.  Placement: after the
 // keys in shared memory when it fits (mask tail excluded), else arenaG.
+template <int T>
 __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* mask, unsigned char* arenaS,
                           int arenaBytes, bool keysInSmem, unsigned char* arenaG, RunArena& A, int* wscr,
                           int pslot = 0) {
@@ -315,7 +329,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     }
   }
   int RR;
-  int r = block_scan_excl(cnt, &RR, wscr);
+  int r = block_scan_excl<T>(cnt, &RR, wscr);
   SLOT_MARK(pslot + 1);
   const int Pmax = RR + E / kPiece;
   HR_CHECK(RR >= nR && RR <= E && RR <= kMaxRuns);
@@ -358,11 +372,11 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   __syncthreads();
   int kcount = 0;
 #pragma unroll
-  for (int u = 0; u < 8; ++u) kcount += __popc(mask[tid * 8 + u]);
+  for (int u = 0; u < 8; ++u) kcount += tid < kLevels ? __popc(mask[tid * 8 + u]) : 0;
   SLOT_MARK(pslot + 3);
   int RK;
-  const int kfirst = block_scan_excl(kcount, &RK, wscr);  // first run slot of bin tid
-  s.keyStart[tid] = kfirst;
+  const int kfirst = block_scan_excl<T>(kcount, &RK, wscr);  // first run slot of bin tid
+  if (tid < kLevels) s.keyStart[tid] = kfirst;
   __syncthreads();
   for (int q = r0; q < r1; ++q) {  // piece count at the run's bin-order slot
     const uint32_t d = runDesc[q];
@@ -376,7 +390,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   int np = 0;  // exclusive scan of the bin-ordered piece counts -> piece offsets
   for (int q = r0; q < r1; ++q) np += (int)slotN[q];
   int P;
-  int off = block_scan_excl(np, &P, wscr);
+  int off = block_scan_excl<T>(np, &P, wscr);
   for (int q = r0; q < r1; ++q) {
     const int n = (int)slotN[q];
     slotN[q] = (uint32_t)off;
@@ -395,7 +409,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     HR_CHECK(p <= P);
   }
   __syncthreads();
-  s.keyStart[tid] = kfirst < RK ? (int)slotN[kfirst] : P;  // run slots -> piece offsets
+  if (tid < kLevels) s.keyStart[tid] = kfirst < RK ? (int)slotN[kfirst] : P;  // run slots -> piece offsets
   if (tid == 0) s.keyStart[kLevels] = P;
   __syncthreads();
   SLOT_MARK(pslot + 6);
@@ -452,6 +466,7 @@ __device__ __forceinline__ double rcp_fast(double x) {
 // K_ac hS_k = hR_a hL_c hS_k / EstRaw_k (Eq. 11); X, Y the evaluated reflectance / illumination.
 // Cells off the supports contribute 0.  Diagnostics only (hr_solve_trace): one more pass over the
 // cells and one block reduction per value; every thread returns the total.
+template <int T>
 __device__ double objective(Sm& s, const hr_params& P, int nR, int nL, double N, const uint8_t* kc,
                             const double* X, const double* Y) {
   const int tid = threadIdx.x;
@@ -473,7 +488,7 @@ __device__ double objective(Sm& s, const hr_params& P, int nR, int nL, double N,
   }
   slot_put3(s, R_OBJ, acc, -1, 0.0, -1, 0.0);
   __syncthreads();
-  const double F = slot_sum(s, R_OBJ);
+  const double F = slot_sum<T>(s, R_OBJ);
   __syncthreads();
   return F;
 }
@@ -488,7 +503,7 @@ __device__ double objective(Sm& s, const hr_params& P, int nR, int nL, double N,
 // kTrace: the Eq. 10 objective trace (hr_solve_trace) is compiled into a separate instance, so
 // the product loop stays small (its body must stay resident in the instruction caches: one CTA
 // per image repeats it T times)
-template <bool kTrace>
+template <int T, bool kTrace>
 __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL, double N, const uint8_t* kc,
                                        const RunArena& A, double* trace = nullptr, int trace_cap = 0) {
   const int tid = threadIdx.x;
@@ -555,25 +570,25 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
     PHASE(0);
     if (t > 0) {  // stop rule (R11) on the renormalised iterates of update t
       const double eps = P.epsilon * N * N;
-      const bool conv = P.use_epsilon && slot_sum(s, R_DR) <= eps && slot_sum(s, R_DL) <= eps;
+      const bool conv = P.use_epsilon && slot_sum<T>(s, R_DR) <= eps && slot_sum<T>(s, R_DL) <= eps;
       if (conv || t >= P.max_iter) break;
     }
     PHASE(14);
     // ======== E2: EstRaw_k over the bin's runs (row order) and their pieces; rho_k (Eq. 11) ========
     {
       const int k = tid;
-      if (s.keyStart[k] < s.keyStart[k + 1]) {
+      if (k < kLevels && s.keyStart[k] < s.keyStart[k + 1]) {
         const double e = bin_sum(s, A, k);  // EstRaw_k (Eqs. 6, 8)
         s.rho[k] = form == 0 ? (e > 0.0 ? s.hSd[k] * rcp_fast(e) : 0.0) : s.hSd[k] * e;
       }
     }
     PHASE(15);
-    const double invDenR = rcp_fast((t == 0 ? slot_sum(s, R_SL2) : cL * cL * QL1) * invN2 + P.beta);
+    const double invDenR = rcp_fast((t == 0 ? slot_sum<T>(s, R_SL2) : cL * cL * QL1) * invN2 + P.beta);
     PHASE(10);
     __syncthreads();
     PHASE(1);
     if (kTrace) {  // before Eq. 13
-      const double F = objective(s, P, nR, nL, N, kc, s.hR, s.hL);
+      const double F = objective<T>(s, P, nR, nL, N, kc, s.hR, s.hL);
       if (tid == 0 && 3 * t < trace_cap) trace[3 * t] = F;
     }
     // ======== R: Eq. 13, TPR threads per row walking every TPR-th cell, fixed-order reduce ========
@@ -624,12 +639,12 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
     __syncthreads();
     PHASE(2);
     if (kTrace) {  // after Eq. 13 (raw hR', current hL)
-      const double F = objective(s, P, nR, nL, N, kc, s.hR1, s.hL);
+      const double F = objective<T>(s, P, nR, nL, N, kc, s.hR1, s.hL);
       if (tid == 0 && 3 * t + 1 < trace_cap) trace[3 * t + 1] = F;
     }
     // ======== L: Eq. 12 (frozen K), TPC threads per column over every TPC-th row ========
     {
-      const double invDenL = rcp_fast(slot_sum(s, R_SR2) * invN2 + P.alpha);
+      const double invDenL = rcp_fast(slot_sum<T>(s, R_SR2) * invN2 + P.alpha);
       double B0 = 0.0, B1 = 0.0;
       const int c = tid >> lgL, p = tid & (TPC - 1);
       if (c < nL) {
@@ -667,13 +682,13 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
     __syncthreads();
     PHASE(3);
     if (kTrace) {  // after Eq. 12 (raw hR', raw hL')
-      const double F = objective(s, P, nR, nL, N, kc, s.hR1, s.hL1);
+      const double F = objective<T>(s, P, nR, nL, N, kc, s.hR1, s.hL1);
       if (tid == 0 && 3 * t + 2 < trace_cap) trace[3 * t + 2] = F;
     }
     ++t;
-    SR1 = slot_sum(s, R_SR1);
-    SL1 = slot_sum(s, R_SL1);
-    QL1 = slot_sum(s, R_QL1);
+    SR1 = slot_sum<T>(s, R_SR1);
+    SL1 = slot_sum<T>(s, R_SL1);
+    QL1 = slot_sum<T>(s, R_QL1);
   }
 #ifdef HR_SOLVE_PROFILE
   if (blockIdx.x == kProfBlock && threadIdx.x == 0)
@@ -687,6 +702,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
 // smraw: solve_smem_bytes() of shared memory; wscr: NW ints of shared scratch.  Every exit is
 // CTA-uniform.  Histograms are read through L2 (__ldcg): in the fused kernel they were
 // accumulated by other CTAs' atomics during this launch.
+template <int T>
 __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t b, unsigned char* smraw, int* wscr) {
 #ifdef HR_SOLVE_PROFILE
   int prof_n = 0;
@@ -702,26 +718,30 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   if (args.only_deferred && args.only_deferred[b] == 0) return;  // solved by k_solve_warp
 
   // ---- histograms (Alg. 1 init) ----
-  s.hSi[tid] = __ldcg(args.hist_s + b * kLevels + tid);
+  constexpr int NW = T / 32;
+  const bool binT = tid < kLevels;  // thread tid <-> bin tid
+  if (binT) s.hSi[tid] = __ldcg(args.hist_s + b * kLevels + tid);
   if (args.hist_g) {
-    s.hGi[tid] = __ldcg(args.hist_g + b * kLevels + tid);
+    if (binT) s.hGi[tid] = __ldcg(args.hist_g + b * kLevels + tid);
   } else {
-    remap_gradient(args.graw + b * kGradSlots, args.grad_norm, s.hGi, wscr);
+    remap_gradient<T>(args.graw + b * kGradSlots, args.grad_norm, s.hGi, wscr);
   }
-  s.bk[tid] = (double)tid / 255.0;
-  s.hSd[tid] = (double)s.hSi[tid];
+  if (binT) {
+    s.bk[tid] = (double)tid / 255.0;
+    s.hSd[tid] = (double)s.hSi[tid];
+  }
   __syncthreads();
   PROF_MARK();
 
   // ---- supports (fixed for all t) ----
-  const bool fL = s.hSi[tid] != 0u, fR = s.hGi[tid] != 0u;
+  const bool fL = binT && s.hSi[tid] != 0u, fR = binT && s.hGi[tid] != 0u;
   int nL, nR;
-  const int pL = block_scan_excl(fL ? 1 : 0, &nL, wscr);
-  const int pR = block_scan_excl(fR ? 1 : 0, &nR, wscr);
+  const int pL = block_scan_excl<T>(fL ? 1 : 0, &nL, wscr);
+  const int pR = block_scan_excl<T>(fR ? 1 : 0, &nR, wscr);
   if (fL) s.listL[pL] = (uint8_t)tid;
   if (fR) s.listR[pR] = (uint8_t)tid;
   {
-    unsigned long long v = s.hSi[tid];
+    unsigned long long v = binT ? s.hSi[tid] : 0ull;
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
     if ((tid & 31) == 0) s.nw[tid >> 5] = v;
@@ -732,10 +752,12 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   for (int u = 0; u < NW; ++u) Nint += s.nw[u];
   const double N = (double)Nint;
   if (Nint == 0 || nR == 0) {  // empty image: zero outputs (never for validated inputs)
-    if (args.hL) args.hL[b * kLevels + tid] = 0.0;
-    if (args.hR) args.hR[b * kLevels + tid] = 0.0;
-    if (args.target) args.target[b * kLevels + tid] = 0.0;
-    if (args.lut) args.lut[b * kLevels + tid] = (uint8_t)tid;
+    if (binT) {
+      if (args.hL) args.hL[b * kLevels + tid] = 0.0;
+      if (args.hR) args.hR[b * kLevels + tid] = 0.0;
+      if (args.target) args.target[b * kLevels + tid] = 0.0;
+      if (args.lut) args.lut[b * kLevels + tid] = (uint8_t)tid;
+    }
     if (tid == 0) {
       if (args.iters) args.iters[b] = 0;
       if (args.status) args.status[b] = HR_EDEGENERATE;
@@ -770,19 +792,19 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   }
   __syncthreads();
   RunArena A;
-  run_build(s, nR, nL, kc, mask, arenaS, AB, keysS, arenaG, A, wscr);
+  run_build<T>(s, nR, nL, kc, mask, arenaS, AB, keysS, arenaG, A, wscr);
   PROF_MARK();
 
   double* tr = args.trace ? args.trace + b * (int64_t)args.trace_stride : nullptr;
-  const int t = tr ? iterate<true>(s, P, nR, nL, N, kc, A, tr, args.trace_stride)
-                  : iterate<false>(s, P, nR, nL, N, kc, A, nullptr, 0);
+  const int t = tr ? iterate<T, true>(s, P, nR, nL, N, kc, A, tr, args.trace_stride)
+                  : iterate<T, false>(s, P, nR, nL, N, kc, A, nullptr, 0);
   if (tr && tid == 0)
     for (int i = 3 * t; i < args.trace_stride; ++i) tr[i] = 0.0;
   PROF_MARK();
 
   // ---- outputs hL, hR (dense, zero off support) ----
-  if (args.hL) args.hL[b * kLevels + tid] = fL ? s.hL[pL] : 0.0;
-  if (args.hR) args.hR[b * kLevels + tid] = fR ? s.hR[pR] : 0.0;
+  if (args.hL && binT) args.hL[b * kLevels + tid] = fL ? s.hL[pL] : 0.0;
+  if (args.hR && binT) args.hR[b * kLevels + tid] = fR ? s.hR[pR] : 0.0;
   if (args.iters && tid == 0) args.iters[b] = t;
 
   // ---- Eq. 20: runs of index_1 (Eqs. 17-19) along each row, summed per bin in row order ----
@@ -794,7 +816,7 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   }
   __syncthreads();
   SLOT_MARK(20);
-  run_build(s, nR, nL, kc1, mask, arenaS, AB, keysS, arenaG, A, wscr, 10);
+  run_build<T>(s, nR, nL, kc1, mask, arenaS, AB, keysS, arenaG, A, wscr, 10);
   for (int p = tid; p < A.P; p += T) {  // piece values hR_a * sum(hL over the piece)
     const uint32_t d = A.pDesc[p];
     const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;
@@ -802,13 +824,13 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   }
   __syncthreads();
   double* Tt = s.rho;  // dense target
-  Tt[tid] = s.keyStart[tid] < s.keyStart[tid + 1] ? bin_sum(s, A, tid) / N : 0.0;
+  if (binT) Tt[tid] = s.keyStart[tid] < s.keyStart[tid + 1] ? bin_sum(s, A, tid) / N : 0.0;
   __syncthreads();
-  if (args.target) args.target[b * kLevels + tid] = Tt[tid];
+  if (args.target && binT) args.target[b * kLevels + tid] = Tt[tid];
   __syncthreads();
   PROF_MARK();
   if (args.lut || args.status)
-    cdf_lut(s.hSi, Tt, s.hL1, s.wgt, s.hL2, wscr, args.lut ? args.lut + b * kLevels : nullptr,
+    cdf_lut<T>(s.hSi, Tt, s.hL1, s.wgt, s.hL2, wscr, args.lut ? args.lut + b * kLevels : nullptr,
             args.status ? args.status + b : nullptr);
 }
 
