@@ -253,8 +253,9 @@ __device__ __forceinline__ void walk_strip(const uint8_t* __restrict__ p, size_t
 // `sm`, then flush them with integer atomics into hist_s_b[256] / hist_graw_b[512].  All NT
 // threads call it; it ends with a barrier (the counters are then free for reuse, not zero).
 // W % 16 == 8 with 8-B aligned rows (VEC 8/9): the last 8 columns of each row are "half strips"
-// walked by their own threads, placed in warps of their own (from the first multiple of 32 past
-// the full-strip threads) so neither kind of warp diverges; one row group fewer when needed.
+// walked by a warp of their own (from the first multiple of 32 past the full-strip threads, up
+// to 32 walkers with row bands of their own, so the warp runs with all lanes busy) so neither
+// kind of warp diverges; fewer full-strip row groups when that leaves < 16 spare threads.
 template <int SW, int VEC, int NT>
 __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, int H, int W, int y0, int y1,
                                              uint32_t* sm, uint32_t* __restrict__ hist_s_b,
@@ -273,9 +274,10 @@ __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, in
   int NG = SPf == 0 ? 0 : (SPf < NT ? NT / SPf : 1);  // row groups
   const bool half = SW == 16 && (VEC == 8 || VEC == 9) && W - xt == 8 && SPf > 0 && SPf < NT;
   if (half)
-    while (NG > 1 && ((NG * SPf + 31) & ~31) + NG > NT) --NG;
+    while (NG > 1 && ((NG * SPf + 31) & ~31) + 16 > NT) --NG;
   const int TH = ((NG * SPf + 31) & ~31);  // first half-strip thread
-  const bool halfOk = half && TH + NG <= NT;
+  const int HT = min(32, NT - TH);         // half-strip walkers: one warp, own row bands
+  const bool halfOk = half && HT >= 16;
   if (halfOk) xt = W;  // no scalar tail
   const int ntile = (SPf + NT - 1) / NT;
   const int grp = SPt ? tid / SPt : 0;
@@ -290,14 +292,15 @@ __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, in
     const int nrows = y1 - y0;
     int RPG = (nrows + NG - 1) / NG;
     if constexpr (VEC == 9) RPG += RPG & 1;  // even: the rows of one step share their parity
-    if (halfOk && tid >= TH) {  // half-strip walkers (whole warps of them, or idle)
+    if (halfOk && tid >= TH) {  // half-strip walkers (a warp of its own, or idle)
       const int g = tid - TH;
-      const int ya = y0 + g * RPG;
-      const int yb = min(y1, ya + RPG);
-      const bool act = g < NG && ya < yb;
+      const int RPH = (nrows + HT - 1) / HT;  // rows per half-strip band (bands of their own)
+      const int ya = y0 + g * RPH;
+      const int yb = min(y1, ya + RPH);
+      const bool act = g < HT && ya < yb;
       const int nr = act ? yb - ya : 0;
       const uint8_t* p = img + (size_t)(act ? ya : 0) * rowBytes + (size_t)(SPf * SW) * 3;
-      walk_strip<2, VEC>(p, rowBytes, RPG, nr, act && yb < H, true, sb, ghi, Lv, Lg);
+      walk_strip<2, VEC>(p, rowBytes, RPH, nr, act && yb < H, true, sb, ghi, Lv, Lg);
     } else {
       for (int tile = 0; tile < ntile; ++tile) {
         const int s = tile * NT + sl;
