@@ -503,7 +503,9 @@ __device__ double objective(Sm& s, const hr_params& P, int nR, int nL, double N,
 // kTrace: the Eq. 10 objective trace (hr_solve_trace) is compiled into a separate instance, so
 // the product loop stays small (its body must stay resident in the instruction caches: one CTA
 // per image repeats it T times)
-template <int T, bool kTrace>
+// kForm: P.update_form as a compile-time constant (each instance carries one form's loops only:
+// a smaller loop body for the instruction caches)
+template <int T, bool kTrace, int kForm>
 __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL, double N, const uint8_t* kc,
                                        const RunArena& A, double* trace = nullptr, int trace_cap = 0) {
   const int tid = threadIdx.x;
@@ -511,7 +513,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
   // covered by the T threads; each group sums its cells in a fixed order (deterministic)
   const int lgR = nR <= T / 8 ? 3 : nR <= T / 4 ? 2 : nR <= T / 2 ? 1 : 0, TPR = 1 << lgR;
   const int lgL = nL <= T / 8 ? 3 : nL <= T / 4 ? 2 : nL <= T / 2 ? 1 : 0, TPC = 1 << lgL;
-  const int form = P.update_form;
+  constexpr int form = kForm;
   const double invN = 1.0 / N, invN2 = invN * invN;
   double SR1 = N, SL1 = N;  // sums of the raw iterates (initially exactly N)
   double QL1 = 0.0;          // sum of the raw hL iterate squared (from the L phase, t > 0)
@@ -796,8 +798,10 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   PROF_MARK();
 
   double* tr = args.trace ? args.trace + b * (int64_t)args.trace_stride : nullptr;
-  const int t = tr ? iterate<T, true>(s, P, nR, nL, N, kc, A, tr, args.trace_stride)
-                  : iterate<T, false>(s, P, nR, nL, N, kc, A, nullptr, 0);
+  const int t = tr ? (P.update_form == 0 ? iterate<T, true, 0>(s, P, nR, nL, N, kc, A, tr, args.trace_stride)
+                                         : iterate<T, true, 1>(s, P, nR, nL, N, kc, A, tr, args.trace_stride))
+              : P.update_form == 0 ? iterate<T, false, 0>(s, P, nR, nL, N, kc, A, nullptr, 0)
+                                   : iterate<T, false, 1>(s, P, nR, nL, N, kc, A, nullptr, 0);
   if (tr && tid == 0)
     for (int i = 3 * t; i < args.trace_stride; ++i) tr[i] = 0.0;
   PROF_MARK();
