@@ -241,6 +241,9 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
                     first) beside the last group's solves; streaming grids sized
                     to the slots the resident solver CTAs leave.  0/1: off;
                     -1: auto = 2 when 2 <= B <= #SMs / 2, else off
+     "group_first_pct" grouped step with 2 groups: the first group's share of  default 38
+                    the batch in % (0: half; a short first histogram pass lets the
+                    first solves hide under the second: C3 0.254 vs 0.261 ms)
      "group_apply"  grouped step's apply: 0 static shares (groups 0..G-2, then     default 0
                     the last group); 1 the last group by CTA tickets
      "solve_wide_px" hr_enhance, one solver CTA per SM (B <= #SMs): 512-thread   default 4194304
