@@ -146,9 +146,9 @@ hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_de
 /* Steps (1)-(4) for the whole batch ("matching its histogram with the one provided by
    HistRetinex") on `stream`.  Default: the histogram, solve + LUT and apply kernels in order,
    chained by programmatic dependent launch, the apply acquiring each image's LUT-ready flag
-   (so it overlaps the solver's tail); for 2 <= B <= #SMs / 2 the grouped step (two image
-   groups, policy "groups": the second group's histograms run beside the first group's solves,
-   the apply beside the second group's solves).  Policy (hr_set_policy): for fused_min_b <= B <=
+   (so it overlaps the solver's tail); for B >= 2 the grouped step (two image groups, policy
+   "groups": the second group's histograms run beside the first group's solves, the apply
+   beside the second group's solves).  Policy (hr_set_policy): for fused_min_b <= B <=
    fused_max_b (fused_min_b = 0 = off by default) with 16-byte aligned buffers and
    H*W % 16 == 0, ONE persistent kernel runs the
    histograms, each image's solve + LUT as soon as its histograms are complete, and the
@@ -240,10 +240,12 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
                     do not wait for them), the apply (every CTA: groups 0..G-2
                     first) beside the last group's solves; streaming grids sized
                     to the slots the resident solver CTAs leave.  0/1: off;
-                    -1: auto = 2 when 2 <= B <= #SMs / 2, else off
-     "group_first_pct" grouped step with 2 groups: the first group's share of  default 38
-                    the batch in % (0: half; a short first histogram pass lets the
-                    first solves hide under the second: C3 0.254 vs 0.261 ms)
+                    -1: auto = 2 when B >= 2
+     "group_first_pct" grouped step with 2 groups: the first group's share of  default -1
+                    the batch in % (0: half; -1: auto = 38 for B <= #SMs / 2, a short
+                    first histogram pass hiding the first solves under the second,
+                    C3 0.254 vs 0.261 ms; 90 for larger batches, the last group's
+                    few solves beside the first group's apply, C5 0.167 vs 0.177)
      "group_apply"  grouped step's apply: 0 static shares (groups 0..G-2, then     default 0
                     the last group); 1 the last group by CTA tickets
      "solve_wide_px" hr_enhance, one solver CTA per SM (B <= #SMs): 512-thread   default 4194304

@@ -46,9 +46,11 @@ struct hr_ctx {
   int solve_wide_px = 4 << 20;  // hr_enhance: 512-thread solver CTAs (one per SM) for H*W >= this (0: never)
   int solve_waves = 0;    // separate kernels, B > SMs: one solver CTA per SM solving images in turn
   int solve_waves_ag = 1; // ... apply CTAs per SM launched beside it
-  int group_first_pct = 38;  // grouped step, G = 2: first group's share of the images in % (0: half):
-                             // a short hist(0) lets solve(0) hide under the longer hist(1)
-                             // (C3: 24 + 40 images 0.254 ms, 32 + 32 0.261 ms)
+  int group_first_pct = -1;  // grouped step, G = 2: first group's share of the images in % (0: half;
+                             // -1: auto = 38 for B <= SMs / 2 -- a short hist(0) lets solve(0) hide
+                             // under the longer hist(1), C3 24 + 40 images 0.254 ms vs 32 + 32 0.261 --
+                             // and 90 for larger batches -- the last group's few solves overlap the
+                             // first group's apply, C5 230 + 26 images 0.167 vs 0.177 ungrouped)
   int groups = -1;        // grouped step (>= 2): histograms of group k+1 run beside the solves of
                           // group k, the apply beside the last group's solves (0/1: off)
   int64_t launches = 0;   // kernels launched through this context (hr_kernel_launches)
@@ -224,7 +226,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_SOLVE_WAVES")) c->solve_waves = atoi(v) != 0;
   if (const char* v = getenv("HR_SOLVE_WIDE_PX")) c->solve_wide_px = atoi(v) >= 0 ? atoi(v) : 4 << 20;
   if (const char* v = getenv("HR_SOLVE_WAVES_AG")) c->solve_waves_ag = atoi(v) == 2 ? 2 : 1;
-  if (const char* v = getenv("HR_GROUP_FIRST_PCT")) c->group_first_pct = atoi(v) >= 0 && atoi(v) < 100 ? atoi(v) : 38;
+  if (const char* v = getenv("HR_GROUP_FIRST_PCT")) c->group_first_pct = atoi(v) >= -1 && atoi(v) < 100 ? atoi(v) : -1;
   if (const char* v = getenv("HR_GROUPS")) c->groups = atoi(v) >= -1 && atoi(v) <= 64 ? atoi(v) : -1;
   *out = c;
   return HR_OK;
@@ -274,7 +276,7 @@ const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
       {"solve_cpsm", &c->solve_cpsm, 0, 2},         {"hist_overlap", &c->hist_overlap, 0, 1},
       {"apply_dyn", &c->apply_dyn, 0, 3},           {"apply_gs", &c->apply_gs, 1, 1 << 20},
       {"hist_tma", &c->hist_tma, 0, 1},             {"groups", &c->groups, -1, 64},
-      {"group_apply", &c->group_apply, 0, 1},       {"group_first_pct", &c->group_first_pct, 0, 99},       {"solve_waves", &c->solve_waves, 0, 1},
+      {"group_apply", &c->group_apply, 0, 1},       {"group_first_pct", &c->group_first_pct, -1, 99},       {"solve_waves", &c->solve_waves, 0, 1},
       {"solve_waves_ag", &c->solve_waves_ag, 1, 2}, {"solve_wide_px", &c->solve_wide_px, 0, 1 << 30},
   };
   for (const Knob& k : knobs)
@@ -574,9 +576,9 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     const char* v = getenv("HR_READY");
     return !(v && atoi(v) == 0);
   }();
-  // groups < 0 (default): 2 groups when B <= SMs / 2 (each group's solves then take at most a
-  // quarter of the CTA slots; C3 0.263 vs 0.270 ms), else off (C5, 256 images: 0.193 vs 0.176)
-  const int ngroups = c->groups >= 0 ? c->groups : (B >= 2 && B <= c->num_sms / 2 ? 2 : 0);
+  // groups < 0 (default): 2 groups for every batch (B >= 2), split by group_first_pct: C3 0.255
+  // vs 0.270 ms ungrouped, C5 0.167 vs 0.177 (equal halves were slower on C5: 0.193)
+  const int ngroups = c->groups >= 0 ? c->groups : (B >= 2 ? 2 : 0);
   if (ngroups >= 2 && B >= 2 && !c->warp_solver && ready_ok) {
     const int64_t G = std::min<int64_t>(ngroups, B);
     uint32_t* ctl = reinterpret_cast<uint32_t*>((char*)ws + L.ctl);
@@ -592,8 +594,8 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     auto gstart = [&](int64_t k) -> int64_t {
       if (k <= 0) return 0;
       if (k >= G) return B;
-      if (G == 2 && c->group_first_pct > 0)
-        return std::min<int64_t>(B - 1, std::max<int64_t>(1, (B * c->group_first_pct + 50) / 100));
+      const int pct = c->group_first_pct >= 0 ? c->group_first_pct : (B <= c->num_sms / 2 ? 38 : 90);
+      if (G == 2 && pct > 0) return std::min<int64_t>(B - 1, std::max<int64_t>(1, (B * pct + 50) / 100));
       return B * k / G;
     };
     const int slots = hist_grid(c);
