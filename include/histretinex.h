@@ -246,8 +246,10 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
                     first histogram pass hiding the first solves under the second,
                     C3 0.254 vs 0.261 ms; 90 for larger batches, the last group's
                     few solves beside the first group's apply, C5 0.167 vs 0.177)
-     "group_apply"  grouped step's apply: 0 static shares (groups 0..G-2, then     default 0
-                    the last group); 1 the last group by CTA tickets
+     "group_apply"  grouped step's apply: 0 static shares (groups 0..G-2, then     default 2
+                    the last group); 1 the last group by CTA tickets through a
+                    shared-memory ring (k_apply_dyn); 2 the last group by CTA tickets
+                    of 8 * apply_gs chunks taken at CTA barriers (k_apply_tma)
      "solve_wide_px" hr_enhance, one solver CTA per SM (B <= #SMs): 512-thread   default 4194304
                     solver CTAs for images of H*W >= value pixels (0: never; large
                     images have large supports: C4 103 vs 121 us per image, while

@@ -41,8 +41,10 @@ struct hr_ctx {
   int hist_tma = 0;       // k_hist: TMA-staged rows where the shape allows (off: measured no faster)
   int hist_overlap = 0;   // separate kernels: solves start per image beside a 2x256-thread histogram pass
                           // (off: the 16-warp histogram pass costs more than the overlap saves)
-  int group_apply = 0;    // grouped step's apply: 0 = static shares of groups 0..G-2, then of the
-                          // last group; 1 = last group by CTA tickets (measured slower)
+  int group_apply = 2;    // grouped step's apply: 0 = static shares of groups 0..G-2, then of the
+                          // last group; 1 = last group by warp-ring CTA tickets (k_apply_dyn,
+                          // measured slower); 2 = last group by CTA tickets taken at barriers
+                          // (k_apply_tma; C3 0.250-0.252 vs 0.254-0.259, C5 0.168 vs 0.168-0.173)
   int solve_wide_px = 4 << 20;  // hr_enhance: 512-thread solver CTAs (one per SM) for H*W >= this (0: never)
   int solve_waves = 0;    // separate kernels, B > SMs: one solver CTA per SM solving images in turn
   int solve_waves_ag = 1; // ... apply CTAs per SM launched beside it
@@ -222,7 +224,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_HIST_TMA")) c->hist_tma = atoi(v) != 0;
   if (const char* v = getenv("HR_APPLY_DYN")) c->apply_dyn = atoi(v) >= 0 && atoi(v) <= 3 ? atoi(v) : 0;
   if (const char* v = getenv("HR_APPLY_GS")) c->apply_gs = atoi(v) > 0 ? atoi(v) : 8;
-  if (const char* v = getenv("HR_GROUP_APPLY")) c->group_apply = atoi(v) != 0;
+  if (const char* v = getenv("HR_GROUP_APPLY")) c->group_apply = atoi(v) >= 0 && atoi(v) <= 2 ? atoi(v) : 2;
   if (const char* v = getenv("HR_SOLVE_WAVES")) c->solve_waves = atoi(v) != 0;
   if (const char* v = getenv("HR_SOLVE_WIDE_PX")) c->solve_wide_px = atoi(v) >= 0 ? atoi(v) : 4 << 20;
   if (const char* v = getenv("HR_SOLVE_WAVES_AG")) c->solve_waves_ag = atoi(v) == 2 ? 2 : 1;
@@ -276,7 +278,7 @@ const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
       {"solve_cpsm", &c->solve_cpsm, 0, 2},         {"hist_overlap", &c->hist_overlap, 0, 1},
       {"apply_dyn", &c->apply_dyn, 0, 3},           {"apply_gs", &c->apply_gs, 1, 1 << 20},
       {"hist_tma", &c->hist_tma, 0, 1},             {"groups", &c->groups, -1, 64},
-      {"group_apply", &c->group_apply, 0, 1},       {"group_first_pct", &c->group_first_pct, -1, 99},       {"solve_waves", &c->solve_waves, 0, 1},
+      {"group_apply", &c->group_apply, 0, 2},       {"group_first_pct", &c->group_first_pct, -1, 99},       {"solve_waves", &c->solve_waves, 0, 1},
       {"solve_waves_ag", &c->solve_waves_ag, 1, 2}, {"solve_wide_px", &c->solve_wide_px, 0, 1 << 30},
   };
   for (const Knob& k : knobs)
@@ -619,7 +621,8 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       e = c->group_apply == 1 && hr::apply_dyn_supported(in, out, B, H, W)
               ? counted(c, hr::launch_apply_dyn(in, lut, B, H, W, out, ag, nullptr, ctl + 3, c->apply_gs, st, ready,
                                                 b_last))
-              : counted(c, hr::launch_apply(in, lut, B, H, W, out, ag, st, ready, b_last));
+              : counted(c, hr::launch_apply(in, lut, B, H, W, out, ag, st, ready, b_last,
+                                            c->group_apply == 2 ? ctl + 3 : nullptr, c->apply_gs));
     if (e == cudaSuccess) e = mark(3);
     return cuda_err(c, e, "hr_enhance");
   }

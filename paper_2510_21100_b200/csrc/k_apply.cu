@@ -27,9 +27,11 @@ namespace {
 
 __global__ void __launch_bounds__(kApplyThreads, 2)
 k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int64_t B, int64_t HW,
-            uint8_t* __restrict__ out, const uint32_t* __restrict__ ready, int64_t b_last) {
+            uint8_t* __restrict__ out, const uint32_t* __restrict__ ready, int64_t b_last,
+            uint32_t* __restrict__ ticket, uint32_t GS) {
   extern __shared__ __align__(128) unsigned char smraw[];
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
+  __shared__ uint32_t tk_s;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   TRACE_T0();
   if (!ready) pdl_wait();  // with per-image flags only the LUTs depend on the solver grid
@@ -42,86 +44,95 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
 
   const uint32_t cpi = (uint32_t)((HW + kChunkPx - 1) / kChunkPx);  // chunks per image
   // chunk space in two parts: images [0, b_last) then [b_last, B) (b_last = B: one part); this
-  // CTA takes a contiguous share of each part, part A first
+  // CTA takes a contiguous share of each part, part A first.  With `ticket`, part B is not
+  // split statically: the CTA takes tickets of kWarps * GS contiguous chunks of it (all warps of
+  // the CTA stream a ticket together, warp w taking chunks w, w + kWarps, ...), so CTAs that
+  // started late or run beside a solver CTA take fewer
   if (b_last <= 0 || b_last > B) b_last = B;
   const uint32_t GA = (uint32_t)(b_last * (int64_t)cpi), GB = (uint32_t)(B * (int64_t)cpi) - GA;  // < 2^31
   const uint32_t a0 = (uint32_t)((uint64_t)GA * blockIdx.x / gridDim.x), a1 = (uint32_t)((uint64_t)GA * (blockIdx.x + 1) / gridDim.x);
-  const uint32_t c0 = GA + (uint32_t)((uint64_t)GB * blockIdx.x / gridDim.x);
-  const uint32_t c1 = GA + (uint32_t)((uint64_t)GB * (blockIdx.x + 1) / gridDim.x);
+  const bool dynB = ticket != nullptr && GB > 0;
+  const uint32_t c0 = GA + (dynB ? 0u : (uint32_t)((uint64_t)GB * blockIdx.x / gridDim.x));
+  const uint32_t c1 = GA + (dynB ? 0u : (uint32_t)((uint64_t)GB * (blockIdx.x + 1) / gridDim.x));
   // this warp's chunks: a0 + w, a0 + w + kWarps, ... < a1, then c0 + w, ... < c1
   auto cnt = [&](uint32_t lo, uint32_t hi) { return (hi - lo > (uint32_t)w) ? (int)((hi - lo - w + kWarps - 1) / kWarps) : 0; };
   const int nA = cnt(a0, a1);
-  const int mine = nA + cnt(c0, c1);
   const uint64_t pol = policy_evict_first();
   uint2* tab = s.tab[w];
   int64_t cur_img = -1;
+  uint32_t nIss = 0, nComp = 0;  // chunks issued / computed by this warp so far (stage and parity)
 
-  // chunk cursor: image b, chunk c within the image; i = this warp's chunk ordinal
-  struct Cur {
-    uint32_t b, c;
-    int i;
-  };
-  auto at = [&](int i) {
-    const uint32_t g = i < nA ? a0 + (uint32_t)w + (uint32_t)i * kWarps : c0 + (uint32_t)w + (uint32_t)(i - nA) * kWarps;
-    return Cur{g / cpi, g % cpi, i};
-  };
-  auto advance = [&](Cur& k) { k = at(k.i + 1); };
-  auto where = [&](const Cur& k, uint64_t& off, uint32_t& bytes) {
-    const uint32_t px0 = k.c * kChunkPx;
+  auto where = [&](uint32_t g, uint64_t& off, uint32_t& bytes, uint32_t& b) {
+    b = g / cpi;
+    const uint32_t px0 = (g - b * cpi) * kChunkPx;
     const uint32_t npx = min((uint32_t)kChunkPx, (uint32_t)(HW - px0));
-    off = ((uint64_t)k.b * (uint64_t)HW + px0) * 3u;
+    off = ((uint64_t)b * (uint64_t)HW + px0) * 3u;
     bytes = npx * 3u;
   };
-  Cur ld = at(0), cp = ld;  // load cursor (lane 0) and compute cursor
-  auto issue = [&](int i) {
+  auto issue = [&](uint32_t g) {  // lane 0
     uint64_t off;
-    uint32_t bytes;
-    where(ld, off, bytes);
-    const int st = i % kStages;
+    uint32_t bytes, b;
+    where(g, off, bytes, b);
+    const int st = (int)(nIss % kStages);
     mbar_expect_tx(&s.bar[w][st], bytes);
     bulk_load(s.stage[w][st], in + off, bytes, &s.bar[w][st], pol);
-    advance(ld);
+    ++nIss;
+  };
+  // this warp's per-chunk pipeline over `count` chunks, chunk i = global chunk index chunk(i)
+  auto pipeline = [&](int count, auto&& chunk) {
+    if (lane == 0)
+      for (int i = 0; i < min(kAhead, count); ++i) issue(chunk(i));
+    for (int i = 0; i < count; ++i) {
+      uint64_t off;
+      uint32_t bytes, b;
+      where(chunk(i), off, bytes, b);
+      if ((int64_t)b != cur_img) {  // per-warp LUT table for this image
+        __syncwarp();
+        if (ready && lane == 0)
+          while (ld_acquire(ready + b) == 0u) __nanosleep(100);
+        __syncwarp();
+        build_tab(tab, lut + (uint64_t)b * kLevels, lane);
+        __syncwarp();
+        cur_img = b;
+      }
+      // prefetch chunk i + kAhead into the stage of chunk i - 2, whose bulk store (committed
+      // two iterations ago) has finished reading shared memory once all but the latest
+      // store group have
+      if (lane == 0 && i + kAhead < count) {
+        if (nComp >= 2) bulk_wait_read<1>();
+        issue(chunk(i + kAhead));
+      }
+      HR_CHECK(bytes > 0 && bytes <= (uint32_t)kChunkBytes && bytes % 48 == 0 && off + bytes <= (uint64_t)B * HW * 3);
+      const int st = (int)(nComp % kStages);
+      mbar_wait(&s.bar[w][st], (nComp / kStages) & 1u);
+      uint8_t* p = s.stage[w][st];
+      apply_chunk_smem(p, bytes, tab, lane);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_store(out + off, p, bytes, pol);
+        bulk_commit();
+      }
+      ++nComp;
+    }
+    if (lane == 0) bulk_wait_read<0>();  // the stages are free for the next call's prologue
+    __syncwarp();
   };
 
-  if (lane == 0)
-    for (int i = 0; i < min(kAhead, mine); ++i) issue(i);
-
-  int st = 0;
-  uint32_t ph = 0;
-  for (int i = 0; i < mine; ++i) {
-    uint64_t off;
-    uint32_t bytes;
-    where(cp, off, bytes);
-    if ((int64_t)cp.b != cur_img) {  // per-warp LUT table for this image
-      __syncwarp();
-      if (ready && lane == 0)
-        while (ld_acquire(ready + cp.b) == 0u) __nanosleep(100);
-      __syncwarp();
-      build_tab(tab, lut + (uint64_t)cp.b * kLevels, lane);
-      __syncwarp();
-      cur_img = cp.b;
-    }
-    // prefetch chunk i + kAhead into the stage of chunk i - 2, whose bulk store (committed
-    // two iterations ago) has finished reading shared memory once all but the latest
-    // store group have
-    if (lane == 0 && i + kAhead < mine) {
-      if (i >= 2) bulk_wait_read<1>();
-      issue(i + kAhead);
-    }
-    HR_CHECK(bytes > 0 && bytes <= (uint32_t)kChunkBytes && bytes % 48 == 0 && off + bytes <= (uint64_t)B * HW * 3);
-    mbar_wait(&s.bar[w][st], ph);
-    uint8_t* p = s.stage[w][st];
-    apply_chunk_smem(p, bytes, tab, lane);
-    fence_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      bulk_store(out + off, p, bytes, pol);
-      bulk_commit();
-    }
-    advance(cp);
-    if (++st == kStages) {
-      st = 0;
-      ph ^= 1u;
+  // static shares: part A, then (without tickets) part B
+  pipeline(nA + cnt(c0, c1), [&](int i) {
+    return i < nA ? a0 + (uint32_t)w + (uint32_t)i * kWarps : c0 + (uint32_t)w + (uint32_t)(i - nA) * kWarps;
+  });
+  if (dynB) {  // part B by CTA tickets
+    const uint32_t CT = (uint32_t)kWarps * GS, nT = (GB + CT - 1) / CT;
+    for (;;) {
+      __syncthreads();
+      if (tid == 0) tk_s = atomicAdd(ticket, 1u);
+      __syncthreads();
+      const uint32_t t = tk_s;
+      if (t >= nT) break;
+      const uint32_t lo = GA + t * CT, hi = min(GA + GB, lo + CT);
+      pipeline(cnt(lo, hi), [&](int i) { return lo + (uint32_t)w + (uint32_t)i * kWarps; });
     }
   }
   if (lane == 0) bulk_wait<0>();
@@ -421,7 +432,8 @@ cudaError_t launch_apply_dyn(const uint8_t* in, const uint8_t* lut, int64_t B, i
 }
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
-                         int grid_ctas, cudaStream_t st, const uint32_t* ready, int64_t b_last) {
+                         int grid_ctas, cudaStream_t st, const uint32_t* ready, int64_t b_last, uint32_t* ticket,
+                         int GS) {
   const int64_t HW = (int64_t)H * W;
   const bool tma = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                    (HW % 16 == 0) && B * ((HW + kChunkPx - 1) / kChunkPx) < (1LL << 31);
@@ -441,7 +453,7 @@ cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32
     if (grid > (chunks + kWarps - 1) / kWarps) grid = (chunks + kWarps - 1) / kWarps;
     if (grid < 1) grid = 1;
     return launch_pdl(k_apply_tma, dim3((unsigned)grid), dim3(kApplyThreads), sizeof(ApplySmem), st, in, lut, B, HW,
-                      out, ready, b_last);
+                      out, ready, b_last, ticket, (uint32_t)(GS < 1 ? 1 : GS));
   } else {
     int64_t grid = 4LL * grid_ctas;
     const int64_t P = B * HW;
