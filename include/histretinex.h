@@ -250,6 +250,8 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
                     the last group); 1 the last group by CTA tickets through a
                     shared-memory ring (k_apply_dyn); 2 the last group by CTA tickets
                     of 8 * apply_gs chunks taken at CTA barriers (k_apply_tma)
+     "apply_tail_pct" grouped step with group_apply 2: % of the first groups'    default 0
+                    chunks also taken by tickets (measured no gain)
      "solve_wide_px" hr_enhance, one solver CTA per SM (B <= #SMs): 512-thread   default 4194304
                     solver CTAs for images of H*W >= value pixels (0: never; large
                     images have large supports: C4 103 vs 121 us per image, while

@@ -48,6 +48,7 @@ struct hr_ctx {
   int solve_wide_px = 4 << 20;  // hr_enhance: 512-thread solver CTAs (one per SM) for H*W >= this (0: never)
   int solve_waves = 0;    // separate kernels, B > SMs: one solver CTA per SM solving images in turn
   int solve_waves_ag = 1; // ... apply CTAs per SM launched beside it
+  int apply_tail_pct = 0;   // grouped step, group_apply 2: % of the first groups' chunks also ticketed
   int group_first_pct = -1;  // grouped step, G = 2: first group's share of the images in % (0: half;
                              // -1: auto = 38 for B <= SMs / 2 -- a short hist(0) lets solve(0) hide
                              // under the longer hist(1), C3 24 + 40 images 0.254 ms vs 32 + 32 0.261 --
@@ -228,6 +229,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_SOLVE_WAVES")) c->solve_waves = atoi(v) != 0;
   if (const char* v = getenv("HR_SOLVE_WIDE_PX")) c->solve_wide_px = atoi(v) >= 0 ? atoi(v) : 4 << 20;
   if (const char* v = getenv("HR_SOLVE_WAVES_AG")) c->solve_waves_ag = atoi(v) == 2 ? 2 : 1;
+  if (const char* v = getenv("HR_APPLY_TAIL_PCT")) c->apply_tail_pct = atoi(v) >= 0 && atoi(v) <= 100 ? atoi(v) : 0;
   if (const char* v = getenv("HR_GROUP_FIRST_PCT")) c->group_first_pct = atoi(v) >= -1 && atoi(v) < 100 ? atoi(v) : -1;
   if (const char* v = getenv("HR_GROUPS")) c->groups = atoi(v) >= -1 && atoi(v) <= 64 ? atoi(v) : -1;
   *out = c;
@@ -278,7 +280,8 @@ const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
       {"solve_cpsm", &c->solve_cpsm, 0, 2},         {"hist_overlap", &c->hist_overlap, 0, 1},
       {"apply_dyn", &c->apply_dyn, 0, 3},           {"apply_gs", &c->apply_gs, 1, 1 << 20},
       {"hist_tma", &c->hist_tma, 0, 1},             {"groups", &c->groups, -1, 64},
-      {"group_apply", &c->group_apply, 0, 2},       {"group_first_pct", &c->group_first_pct, -1, 99},       {"solve_waves", &c->solve_waves, 0, 1},
+      {"group_apply", &c->group_apply, 0, 2},       {"group_first_pct", &c->group_first_pct, -1, 99},
+      {"apply_tail_pct", &c->apply_tail_pct, 0, 100},       {"solve_waves", &c->solve_waves, 0, 1},
       {"solve_waves_ag", &c->solve_waves_ag, 1, 2}, {"solve_wide_px", &c->solve_wide_px, 0, 1 << 30},
   };
   for (const Knob& k : knobs)
@@ -622,7 +625,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
               ? counted(c, hr::launch_apply_dyn(in, lut, B, H, W, out, ag, nullptr, ctl + 3, c->apply_gs, st, ready,
                                                 b_last))
               : counted(c, hr::launch_apply(in, lut, B, H, W, out, ag, st, ready, b_last,
-                                            c->group_apply == 2 ? ctl + 3 : nullptr, c->apply_gs));
+                                            c->group_apply == 2 ? ctl + 3 : nullptr, c->apply_gs, c->apply_tail_pct));
     if (e == cudaSuccess) e = mark(3);
     return cuda_err(c, e, "hr_enhance");
   }

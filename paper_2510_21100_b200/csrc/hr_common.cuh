@@ -215,7 +215,7 @@ cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B
 // does not wait for the solver grid to finish but acquires ready[b] before image b's table
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W,
                          uint8_t* out, int grid_ctas, cudaStream_t st, const uint32_t* ready = nullptr,
-                         int64_t b_last = 0, uint32_t* ticket = nullptr, int GS = 8);
+                         int64_t b_last = 0, uint32_t* ticket = nullptr, int GS = 8, int tail_pct = 0);
 // b_last (0 < b_last < B): every CTA first takes its share of images [0, b_last), then its share
 // of [b_last, B) (the grouped step: the last group's LUTs complete last); with ticket (zeroed
 // counter), images [b_last, B) go by CTA tickets of 8 * GS chunks instead of static shares

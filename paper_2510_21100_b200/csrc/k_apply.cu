@@ -28,7 +28,7 @@ namespace {
 __global__ void __launch_bounds__(kApplyThreads, 2)
 k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int64_t B, int64_t HW,
             uint8_t* __restrict__ out, const uint32_t* __restrict__ ready, int64_t b_last,
-            uint32_t* __restrict__ ticket, uint32_t GS) {
+            uint32_t* __restrict__ ticket, uint32_t GS, uint32_t tail_pct) {
   extern __shared__ __align__(128) unsigned char smraw[];
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
   __shared__ uint32_t tk_s;
@@ -49,9 +49,12 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   // the CTA stream a ticket together, warp w taking chunks w, w + kWarps, ...), so CTAs that
   // started late or run beside a solver CTA take fewer
   if (b_last <= 0 || b_last > B) b_last = B;
-  const uint32_t GA = (uint32_t)(b_last * (int64_t)cpi), GB = (uint32_t)(B * (int64_t)cpi) - GA;  // < 2^31
+  const uint32_t GA0 = (uint32_t)(b_last * (int64_t)cpi), GB0 = (uint32_t)(B * (int64_t)cpi) - GA0;  // < 2^31
+  const bool dynB = ticket != nullptr && GB0 > 0;
+  // with tickets, the last tail_pct % of part A joins the ticketed part (natural order)
+  const uint32_t GA = dynB ? GA0 - (uint32_t)((uint64_t)GA0 * min(tail_pct, 100u) / 100u) : GA0;
+  const uint32_t GB = GA0 + GB0 - GA;
   const uint32_t a0 = (uint32_t)((uint64_t)GA * blockIdx.x / gridDim.x), a1 = (uint32_t)((uint64_t)GA * (blockIdx.x + 1) / gridDim.x);
-  const bool dynB = ticket != nullptr && GB > 0;
   const uint32_t c0 = GA + (dynB ? 0u : (uint32_t)((uint64_t)GB * blockIdx.x / gridDim.x));
   const uint32_t c1 = GA + (dynB ? 0u : (uint32_t)((uint64_t)GB * (blockIdx.x + 1) / gridDim.x));
   // this warp's chunks: a0 + w, a0 + w + kWarps, ... < a1, then c0 + w, ... < c1
@@ -433,7 +436,7 @@ cudaError_t launch_apply_dyn(const uint8_t* in, const uint8_t* lut, int64_t B, i
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
                          int grid_ctas, cudaStream_t st, const uint32_t* ready, int64_t b_last, uint32_t* ticket,
-                         int GS) {
+                         int GS, int tail_pct) {
   const int64_t HW = (int64_t)H * W;
   const bool tma = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                    (HW % 16 == 0) && B * ((HW + kChunkPx - 1) / kChunkPx) < (1LL << 31);
@@ -453,7 +456,7 @@ cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32
     if (grid > (chunks + kWarps - 1) / kWarps) grid = (chunks + kWarps - 1) / kWarps;
     if (grid < 1) grid = 1;
     return launch_pdl(k_apply_tma, dim3((unsigned)grid), dim3(kApplyThreads), sizeof(ApplySmem), st, in, lut, B, HW,
-                      out, ready, b_last, ticket, (uint32_t)(GS < 1 ? 1 : GS));
+                      out, ready, b_last, ticket, (uint32_t)(GS < 1 ? 1 : GS), (uint32_t)(tail_pct < 0 ? 0 : tail_pct));
   } else {
     int64_t grid = 4LL * grid_ctas;
     const int64_t P = B * HW;
