@@ -252,6 +252,9 @@ hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
                     of 8 * apply_gs chunks taken at CTA barriers (k_apply_tma)
      "apply_tail_pct" grouped step with group_apply 2: % of the first groups'    default 0
                     chunks also taken by tickets (measured no gain)
+     "solve_queue"  grouped step: each solver CTA takes the next image in the     default 0
+                    order the histograms complete (a queue k_hist fills) instead of
+                    its own image (measured no gain: the apply still goes in image order)
      "solve_wide_px" hr_enhance, one solver CTA per SM (B <= #SMs): 512-thread   default 4194304
                     solver CTAs for images of H*W >= value pixels (0: never; large
                     images have large supports: C4 103 vs 121 us per image, while

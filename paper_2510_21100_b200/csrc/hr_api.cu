@@ -41,6 +41,7 @@ struct hr_ctx {
   int hist_tma = 0;       // k_hist: TMA-staged rows where the shape allows (off: measured no faster)
   int hist_overlap = 0;   // separate kernels: solves start per image beside a 2x256-thread histogram pass
                           // (off: the 16-warp histogram pass costs more than the overlap saves)
+  int solve_queue = 0;    // grouped step: solver CTAs take images in histogram-completion order
   int group_apply = 2;    // grouped step's apply: 0 = static shares of groups 0..G-2, then of the
                           // last group; 1 = last group by warp-ring CTA tickets (k_apply_dyn,
                           // measured slower); 2 = last group by CTA tickets taken at barriers
@@ -225,6 +226,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   if (const char* v = getenv("HR_HIST_TMA")) c->hist_tma = atoi(v) != 0;
   if (const char* v = getenv("HR_APPLY_DYN")) c->apply_dyn = atoi(v) >= 0 && atoi(v) <= 3 ? atoi(v) : 0;
   if (const char* v = getenv("HR_APPLY_GS")) c->apply_gs = atoi(v) > 0 ? atoi(v) : 8;
+  if (const char* v = getenv("HR_SOLVE_QUEUE")) c->solve_queue = atoi(v) != 0;
   if (const char* v = getenv("HR_GROUP_APPLY")) c->group_apply = atoi(v) >= 0 && atoi(v) <= 2 ? atoi(v) : 2;
   if (const char* v = getenv("HR_SOLVE_WAVES")) c->solve_waves = atoi(v) != 0;
   if (const char* v = getenv("HR_SOLVE_WIDE_PX")) c->solve_wide_px = atoi(v) >= 0 ? atoi(v) : 4 << 20;
@@ -281,7 +283,7 @@ const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
       {"apply_dyn", &c->apply_dyn, 0, 3},           {"apply_gs", &c->apply_gs, 1, 1 << 20},
       {"hist_tma", &c->hist_tma, 0, 1},             {"groups", &c->groups, -1, 64},
       {"group_apply", &c->group_apply, 0, 2},       {"group_first_pct", &c->group_first_pct, -1, 99},
-      {"apply_tail_pct", &c->apply_tail_pct, 0, 100},       {"solve_waves", &c->solve_waves, 0, 1},
+      {"apply_tail_pct", &c->apply_tail_pct, 0, 100}, {"solve_queue", &c->solve_queue, 0, 1},       {"solve_waves", &c->solve_waves, 0, 1},
       {"solve_waves_ag", &c->solve_waves_ag, 1, 2}, {"solve_wide_px", &c->solve_wide_px, 0, 1 << 30},
   };
   for (const Knob& k : knobs)
@@ -490,8 +492,11 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   };
   auto solve_chunk = [&](int64_t b0, int64_t nb, cudaStream_t s, uint32_t* ready = nullptr,
                          const uint32_t* hist_done = nullptr, int hist_bands = 0, uint32_t* queue = nullptr,
-                         uint32_t* queue_tail = nullptr, int cpsm = 0, int max_ctas = 0) -> cudaError_t {
+                         uint32_t* queue_tail = nullptr, int cpsm = 0, int max_ctas = 0,
+                         const uint32_t* cq = nullptr, uint32_t* cq_head = nullptr) -> cudaError_t {
     hr::SolveArgs a{};
+    a.cq = c->warp_solver ? nullptr : cq;
+    a.cq_head = cq_head;
     a.ready = c->warp_solver ? nullptr : ready;
     a.queue = c->warp_solver ? nullptr : queue;
     a.queue_tail = queue_tail;
@@ -608,9 +613,13 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     for (int64_t k = 0; k < G && e == cudaSuccess; ++k) {
       const int64_t b0 = gstart(k), nb = gstart(k + 1) - b0;
       const int grid = (int)std::max<int64_t>(c->num_sms, slots - std::min<int64_t>(prev_nb, slots / 2));
+      // histogram-completion queue of this group (solver CTAs take images in the order they complete)
+      uint32_t* cq = c->solve_queue ? ctl + hr::kCtlHeader + 3 * B + b0 : nullptr;
+      uint32_t* cqc = ctl + hr::kCtlHeader + 4 * B + 2 * k;  // [0] tail, [1] head
       e = counted(c, hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, grid, st,
-                                     hr::kHistThreads, done + b0, 0, k > 0));
-      if (e == cudaSuccess) e = solve_chunk(b0, nb, st, ready + b0, done + b0, 0, nullptr, nullptr, 2);
+                                     hr::kHistThreads, done + b0, 0, k > 0, cq, cq ? cqc : nullptr));
+      if (e == cudaSuccess)
+        e = solve_chunk(b0, nb, st, ready + b0, done + b0, 0, nullptr, nullptr, 2, 0, cq, cq ? cqc + 1 : nullptr);
       prev_nb = nb;
     }
     if (e == cudaSuccess) e = mark(2);

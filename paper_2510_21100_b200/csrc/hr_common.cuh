@@ -151,7 +151,10 @@ constexpr int kApplyThreads = 256;
 // (hist_wave_images), leaving registers and shared memory for one solver CTA per SM
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
                         uint32_t* hist_graw, int grid, cudaStream_t st, int nt = kHistThreads,
-                        uint32_t* done = nullptr, int tma = 1, bool nowait = false);
+                        uint32_t* done = nullptr, int tma = 1, bool nowait = false, uint32_t* cq = nullptr,
+                        uint32_t* cq_tail = nullptr);
+// cq, cq_tail (with done; direct-load kernel): the segment that completes image b appends b + 1
+// to cq at atomicAdd(cq_tail) (release), i.e. images in histogram-completion order
 // nowait: the kernel does not wait for its stream predecessor (griddepcontrol.wait); only for a
 // predecessor it shares no data with (the grouped step's histograms of group k >= 1 follow the
 // solver of group k - 1)
@@ -195,6 +198,8 @@ struct SolveArgs {
   int32_t trace_stride;
   int64_t nimg;                  // > 0: images solved by a grid of fewer CTAs (CTA c: c, c + grid, ...);
                                  // 0: one image per CTA
+  const uint32_t* cq;            // nullable (with hist_done): histogram-completion queue (k_hist); each
+  uint32_t* cq_head;             // CTA solves the image at cq[atomicAdd(cq_head)] - 1 (acquire)
 };
 // warp-per-image solver for nR <= 32; flags the other images in deferred[b] (then run k_solve)
 cudaError_t launch_solve_warp(const SolveArgs& a, int64_t B, int32_t* deferred, cudaStream_t st);
@@ -239,7 +244,9 @@ cudaError_t launch_zero(void* p, size_t n, cudaStream_t st);
 constexpr int kCtlHeader = 32;  // control words before done[B]
 // control block: [header | done[B] | ready[B] | queue[B]]; header word 2 = completion-queue
 // tail, word 3 = dynamic-apply ticket
-inline size_t fused_ctl_bytes(int64_t B) { return (size_t)(kCtlHeader + 3 * B) * sizeof(uint32_t); }
+// control block: header, done[B], ready[B], LUT queue[B], histogram-completion queue[B], and per
+// group (<= 64) the completion queue's tail and head counters
+inline size_t fused_ctl_bytes(int64_t B) { return (size_t)(kCtlHeader + 4 * B + 128) * sizeof(uint32_t); }
 struct FusedArgs {
   const uint8_t* in;  // [B][H][W][3]
   uint8_t* out;       // [B][H][W][3]

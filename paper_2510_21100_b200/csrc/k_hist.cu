@@ -362,7 +362,8 @@ cudaError_t launch_tma(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint
 template <int SW, int VEC, int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT)
 k_hist(const uint8_t* __restrict__ rgb, int64_t B, int H, int W, uint32_t* __restrict__ hist_s,
-       uint32_t* __restrict__ hist_graw, uint32_t* __restrict__ done, int nowait) {
+       uint32_t* __restrict__ hist_graw, uint32_t* __restrict__ done, int nowait, uint32_t* __restrict__ cq,
+       uint32_t* __restrict__ cq_tail) {
   extern __shared__ __align__(16) uint32_t sm[];
   TRACE_T0();
   if (!nowait) pdl_wait();
@@ -382,7 +383,11 @@ k_hist(const uint8_t* __restrict__ rgb, int64_t B, int H, int W, uint32_t* __res
                               hist_graw + b * kGradSlots);
     if (done) {
       __threadfence();
-      if (threadIdx.x == 0) atomicAdd(done + b, (uint32_t)(y1 - y0));
+      if (threadIdx.x == 0) {
+        const uint32_t rows = (uint32_t)(y1 - y0);
+        // the segment that completes image b appends it to the completion queue (release)
+        if (atomicAdd(done + b, rows) + rows == (uint32_t)H && cq) st_release(cq + atomicAdd(cq_tail, 1u), (uint32_t)b + 1u);
+      }
     }
   }
   TRACE_END(1u, (uint32_t)((uintptr_t)hist_s >> 8), 0ull);  // aux: which launch (group)
@@ -390,7 +395,7 @@ k_hist(const uint8_t* __restrict__ rgb, int64_t B, int H, int W, uint32_t* __res
 
 template <int SW, int VEC, int NT>
 cudaError_t launch_v(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hs, uint32_t* hg, int grid,
-                     uint32_t* done, cudaStream_t st, bool nowait) {
+                     uint32_t* done, cudaStream_t st, bool nowait, uint32_t* cq, uint32_t* cq_tail) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
@@ -399,14 +404,14 @@ cudaError_t launch_v(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32
     attr = true;
   }
   return launch_pdl(k_hist<SW, VEC, NT>, dim3(grid), dim3(NT), kHistDevSmem, st, rgb, B, H, W, hs, hg, done,
-                    (int)nowait);
+                    (int)nowait, cq, cq_tail);
 }
 
 template <int SW, int VEC>
 cudaError_t launch_nt(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hs, uint32_t* hg, int grid,
-                      int nt, uint32_t* done, cudaStream_t st, bool nowait) {
-  return nt == 256 ? launch_v<SW, VEC, 256>(rgb, B, H, W, hs, hg, grid, done, st, nowait)
-                   : launch_v<SW, VEC, kHistThreads>(rgb, B, H, W, hs, hg, grid, done, st, nowait);
+                      int nt, uint32_t* done, cudaStream_t st, bool nowait, uint32_t* cq, uint32_t* cq_tail) {
+  return nt == 256 ? launch_v<SW, VEC, 256>(rgb, B, H, W, hs, hg, grid, done, st, nowait, cq, cq_tail)
+                   : launch_v<SW, VEC, kHistThreads>(rgb, B, H, W, hs, hg, grid, done, st, nowait, cq, cq_tail);
 }
 
 bool hist_w8_strip16() {  // measurement switch: HR_HIST_W8=8 keeps the 8-px strips
@@ -466,9 +471,9 @@ int hist_grid_clamped(int64_t B, int32_t H, int grid) {
 
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
                         uint32_t* hist_graw, int grid, cudaStream_t st, int nt, uint32_t* done, int tma,
-                        bool nowait) {
+                        bool nowait, uint32_t* cq, uint32_t* cq_tail) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(rgb);
-  if (tma && !nowait && tma_hist_supported(rgb, B, H, W)) {
+  if (tma && !nowait && !cq && tma_hist_supported(rgb, B, H, W)) {
     // TMA-staged kernel: one CTA per SM (grid is given for 2 CTAs per SM)
     const int g1 = hist_grid_clamped(B, H, std::max(1, grid / 2));
     if (done) {  // overlapped with the solver: 512 threads, <= 64 registers, image waves
@@ -480,13 +485,13 @@ cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uin
                                                : launch_tma<8>(rgb, B, H, W, hist_s, hist_graw, g1, st);
   }
   grid = hist_grid_clamped(B, H, grid);
-  if (a % 16 == 0 && W % 16 == 0) return launch_nt<16, 16>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait);
+  if (a % 16 == 0 && W % 16 == 0) return launch_nt<16, 16>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait, cq, cq_tail);
   // 8-B aligned rows: 16-px strips of six 8-B loads (the W % 16 == 8 remainder is the scalar tail)
   if (a % 8 == 0 && W % 8 == 0 && W >= 16 && hist_w8_strip16())
-    return hist_mixed() ? launch_nt<16, 9>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait)
-                        : launch_nt<16, 8>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait);
-  if (a % 8 == 0 && W % 8 == 0) return launch_nt<8, 8>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait);
-  return launch_nt<16, 1>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait);
+    return hist_mixed() ? launch_nt<16, 9>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait, cq, cq_tail)
+                        : launch_nt<16, 8>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait, cq, cq_tail);
+  if (a % 8 == 0 && W % 8 == 0) return launch_nt<8, 8>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait, cq, cq_tail);
+  return launch_nt<16, 1>(rgb, B, H, W, hist_s, hist_graw, grid, nt, done, st, nowait, cq, cq_tail);
 }
 
 }  // namespace hr

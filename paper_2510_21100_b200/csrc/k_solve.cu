@@ -27,8 +27,23 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_solve(SolveArgs args) {
   }
   // one image per CTA, or (nimg > 0) images blockIdx.x, blockIdx.x + gridDim.x, ... in turn
   const int64_t n = args.nimg > 0 ? args.nimg : (int64_t)gridDim.x;
-  for (int64_t b = blockIdx.x; b < n; b += gridDim.x) {
-    if (args.hist_done) {  // overlap the histogram pass: wait for this image's rows only
+  __shared__ int64_t b_s;
+  for (int64_t bi = blockIdx.x; bi < n; bi += gridDim.x) {
+    int64_t b = bi;
+    if (args.cq) {  // the next image in histogram-completion order (complete by construction)
+      if (threadIdx.x == 0) {
+        const uint32_t pos = atomicAdd(args.cq_head, 1u);
+        uint32_t v;
+        long long spins = 0;
+        while ((v = ld_acquire(args.cq + pos)) == 0u) {
+          __nanosleep(128);
+          if (++spins > (1LL << 25)) asm volatile("trap;");  // ~10 s: a logic error, not a wait
+        }
+        b_s = (int64_t)v - 1;
+      }
+      __syncthreads();
+      b = b_s;
+    } else if (args.hist_done) {  // overlap the histogram pass: wait for this image's rows only
       if (threadIdx.x == 0) {
         const uint32_t need = (uint32_t)args.hist_H;
         long long spins = 0;

@@ -155,7 +155,8 @@ def test_enhance_host_rejects_bad_args():
                                   "solve_waves", "solve_waves,solve_waves_ag=2", "solve_wide_px=1",
                                   "groups=2,group_first_pct=0", "groups=2,group_first_pct=99",
                                   "groups=2,group_apply=2", "groups=3,group_apply=2,apply_gs=1",
-                                  "groups=2,apply_tail_pct=30", "groups=2,apply_tail_pct=100"])
+                                  "groups=2,apply_tail_pct=30", "groups=2,apply_tail_pct=100",
+                                  "solve_queue", "groups=3,solve_queue"])
 @pytest.mark.parametrize("shape", [(2, 4, 4), (3, 37, 112), (4, 30, 24), (40, 16, 32), (300, 8, 16), (2, 37, 101),
                                    (2, 37, 264), (20, 45, 256), (5, 120, 600), (1, 300, 1920), (150, 16, 256)])
 def test_policy_options_bit_exact(knob, shape):
