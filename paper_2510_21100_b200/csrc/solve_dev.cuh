@@ -818,17 +818,55 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
     const int a = e / nL, c = e - a * nL;
     kc1[e] = __ldg(args.idx1_tab + s.listR[a] * kLevels + s.listL[c]);
   }
+  // index_1 is non-decreasing along a row (b_i p_j increases with j), so row a's keys cover the
+  // range [kmin_a, kmax_a]; D holds, per row, hR_a * (sum of hL over the cells of key k) for k in
+  // that range (zero where no cell has key k), rows at offsets rowOff[a] (a block scan of the
+  // widths).  Then T_k = (1/N) sum over the rows, in row order, of D[a][k]: deterministic, and no
+  // run/piece structure to build (that build cost more than the sums themselves).
+  int* rowOff = s.keyStart;                          // the iteration's bin offsets are dead now
+  uint8_t* kmin = reinterpret_cast<uint8_t*>(mask);  // so is the bin row mask
   __syncthreads();
   SLOT_MARK(20);
-  run_build<T>(s, nR, nL, kc1, mask, arenaS, AB, keysS, arenaG, A, wscr, 10);
-  for (int p = tid; p < A.P; p += T) {  // piece values hR_a * sum(hL over the piece)
-    const uint32_t d = A.pDesc[p];
-    const int lo = d & 255, hi = (d >> 8) & 255, pa = d >> 16;
-    A.pVal[p] = s.hR[pa] * piece_sum(s.hL, lo, hi);
+  const int wr = tid < nR ? (int)kc1[tid * nL + nL - 1] - (int)kc1[tid * nL] + 1 : 0;
+  int Wtot;
+  const int offr = block_scan_excl<T>(wr, &Wtot, wscr);
+  if (tid < nR) {
+    rowOff[tid] = offr;
+    kmin[tid] = kc1[tid * nL];
+  }
+  const bool dS = keysS && align16(E) + 8 * Wtot <= AB - kMaskBytes;
+  double* D = dS ? reinterpret_cast<double*>(arenaS + align16(E)) : reinterpret_cast<double*>(arenaG);
+  HR_CHECK(dS || 8 * Wtot <= 12 * kMaxPieces);
+  for (int i = tid; i < Wtot; i += T) D[i] = 0.0;
+  __syncthreads();
+  if (tid < nR) {  // row a = tid: its runs in order
+    const uint8_t* kr = kc1 + tid * nL;
+    const int k0 = kr[0];
+    double acc = 0.0;
+    int k = k0;
+    for (int c = 0; c < nL; ++c) {
+      const int kn = kr[c];
+      HR_CHECK(kn >= k);
+      if (kn != k) {
+        D[offr + k - k0] = s.hR[tid] * acc;
+        acc = 0.0;
+        k = kn;
+      }
+      acc += s.hL[c];
+    }
+    D[offr + k - k0] = s.hR[tid] * acc;
   }
   __syncthreads();
   double* Tt = s.rho;  // dense target
-  if (binT) Tt[tid] = s.keyStart[tid] < s.keyStart[tid + 1] ? bin_sum(s, A, tid) / N : 0.0;
+  if (binT) {
+    double e0 = 0.0;
+    for (int a = 0; a < nR; ++a) {
+      const int j = tid - (int)kmin[a];
+      const int w = (a + 1 < nR ? rowOff[a + 1] : Wtot) - rowOff[a];
+      if (j >= 0 && j < w) e0 += D[rowOff[a] + j];
+    }
+    Tt[tid] = e0 / N;
+  }
   __syncthreads();
   if (args.target && binT) args.target[b * kLevels + tid] = Tt[tid];
   __syncthreads();
