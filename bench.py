@@ -17,6 +17,13 @@ Multi-GPU (torchrun, one process per GPU): every rank enhances its own batch (we
 data-path collective -- images are independent); the step time is the max over ranks
 (all_reduce MAX of the device-event time).  `--impl reference` times the CPU oracle (the only
 reference this paper-only tier has) on the host cores; only rank 0 runs it.
+
+The line reports, besides the contract keys: `timing` (>= 50 individually timed replays spanning
+>= 1 s: median, p10, p90; nvidia-smi clocks are sampled over the timed region and the replays),
+`in_step` (each kernel launch's start/end inside one step of the timed schedule, from the
+library's %globaltimer step trace), `roofline` for the unit launched per step (hr_enhance: its
+kernels overlap), the separate-kernel stage split as information, `cpu_baseline` (oracle on all
+host threads, on one core, and per stage).
 """
 from __future__ import annotations
 
@@ -156,13 +163,13 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
-def oracle_sample(cfg: str, x, p_oracle, budget_s: float = 12.0):
+def oracle_sample(cfg: str, x, p_oracle, budget_s: float = 12.0, max_threads: int = 0):
     """Time the oracle (as it stands) on a bounded sample of the workload on the host cores:
     about `budget_s` seconds of wall time on all cores (images of the batch, repeated in whole
     passes when the batch is smaller).  Returns (MP/s, cores, description)."""
     import oracle
 
-    cores = cpu_cores()
+    cores = cpu_cores() if max_threads <= 0 else min(max_threads, cpu_cores())
     B = x.shape[0]
     t0 = time.perf_counter()  # one image on one core sizes the sample
     oracle.enhance_batch(x[:1], p_oracle, nthreads=1, want_out=True)
@@ -241,8 +248,106 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, world, rank, local):
+REC_DTYPE = None  # numpy dtype of hr_trace_bind records (set lazily)
+KIND = {1: "k_hist", 3: "k_solve", 4: "k_apply"}
+
+
+def trace_step(hr, step, local, B, H, W, dev):
+    """In-step kernel durations of the timed schedule (hr_trace_bind, %globaltimer): the second
+    of two back-to-back steps; per launch its first CTA start and last CTA end relative to the
+    step's first CTA, and the rate of the streaming launches over their span."""
     import numpy as np
+    import torch
+
+    global REC_DTYPE
+    REC_DTYPE = np.dtype([("kind", "<u4"), ("cta", "<u4"), ("sm", "<u4"), ("aux", "<u4"), ("t0", "<u8"),
+                          ("mid", "<u8"), ("t1", "<u8"), ("pad", "<u8")])
+    cap = 1 << 16
+    buf = torch.zeros(cap * REC_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    spans = []
+    for rep in range(5):
+        step()
+        torch.cuda.synchronize(dev)
+        hr.trace_bind(buf, cnt, cap, local)
+        step()
+        torch.cuda.synchronize(dev)
+        hr.trace_bind(None, None, 0, local)
+        n = min(int(cnt.item()), cap)
+        cnt.zero_()
+        r = np.frombuffer(buf.cpu().numpy().tobytes(), dtype=REC_DTYPE)[:n]
+        if n == 0:
+            return None
+        T0 = int(r["t0"].min())
+        launches = []
+        for k in (1, 3, 4):
+            q = r[r["kind"] == k]
+            for aux in sorted(set(q["aux"].tolist()), key=lambda a: int(q[q["aux"] == a]["t0"].min())):
+                z = q[q["aux"] == aux]
+                launches.append((KIND[k], len(z), (int(z["t0"].min()) - T0) / 1e3, (int(z["t1"].max()) - T0) / 1e3))
+        spans.append(((int(r["t1"].max()) - T0) / 1e3, launches))
+    spans.sort(key=lambda s: s[0])
+    span, launches = spans[len(spans) // 2]  # the median step of five
+    out = {"step_span_us": round(span, 1), "launches": [],
+           "note": "median of 5 traced steps; %globaltimer per CTA (hr_trace_bind), times from the step's first CTA"}
+    for name, ctas, t0, t1 in launches:
+        out["launches"].append({"kernel": name, "ctas": ctas, "start_us": round(t0, 1), "end_us": round(t1, 1),
+                                "span_us": round(t1 - t0, 1)})
+    return out
+
+
+def oracle_stages(x, p_oracle):
+    """Per-stage wall times of the oracle on one image, one core (SPEC BenchRecord stages):
+    histograms, Algorithm 1, Eqs. 17-20, matching LUT, pixel reconstruction."""
+    import numpy as np
+
+    import oracle
+
+    img = x[0]
+    t = {}
+    t0 = time.perf_counter()
+    S = oracle.value_channel(img)
+    G = oracle.gradient_levels(oracle.gradient_raw(S), 256, p_oracle.grad_norm)
+    hS, hG = oracle.count_histogram(S, 256), oracle.count_histogram(G, 256)
+    t["histograms"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    hL, hR, it, _ = oracle.decompose(hS, hG, p_oracle)
+    t["algorithm1"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    T = oracle.enhanced_histogram(hR, hL, oracle.index_map(256, p_oracle.gamma), float(hS.sum()))
+    t["eq17_20"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    lut = oracle.match_lut(hS, T)
+    t["match_lut"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.reconstruct(img, lut[S])
+    t["apply"] = time.perf_counter() - t0
+    return {k: round(v * 1e3, 3) for k, v in t.items()} | {"unit": "ms per image, 1 core",
+                                                           "image": f"{img.shape[1]}x{img.shape[0]}"}
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def pct(a, q):
+    a = sorted(a)
+    if not a:
+        return None
+    i = (len(a) - 1) * q / 100.0
+    lo = int(i)
+    hi = min(lo + 1, len(a) - 1)
+    return a[lo] + (a[hi] - a[lo]) * (i - lo)
+
+
+def run_ours(args, world, rank, local):
     import torch
 
     import paper_2510_21100_b200 as hr
@@ -275,77 +380,83 @@ def run_ours(args, world, rank, local):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize(dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev) if flush_l2(B, H, W) else None
 
-    # ---- device-resident timed region: the product path, nothing recorded between kernels
-    # (events between kernels would break the programmatic-dependent-launch chain) ----
+    def timed_steps(n):
+        """n steps; per-step events (after an L2 flush outside the interval when the input fits in
+        L2), or one interval around n back-to-back steps.  Returns (ms per step, [per-step ms])."""
+        if flush is not None:
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+            for a, b in ev:
+                flush.fill_(1)
+                a.record(stream)
+                step()
+                b.record(stream)
+            torch.cuda.synchronize(dev)
+            per = [a.elapsed_time(b) for a, b in ev]
+            return sum(per) / n, per
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / n, None
+
+    # ---- the timed region: exactly K steps of the product path, device-resident inputs;
+    # nothing is recorded between the kernels of a step (events would break the PDL chain) ----
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     launches0 = hr.kernel_launches(local)
-    if flush_l2(B, H, W):
-        # inputs smaller than L2: every step is timed on its own, after an L2 flush (a 256 MB
-        # device write) that is outside the timed interval
-        flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        launches0 = hr.kernel_launches(local)
-        for a, b in ev:
-            flush.fill_(1)
-            a.record(stream)
-            step()
-            b.record(stream)
-        torch.cuda.synchronize(dev)
-        launches = hr.kernel_launches(local) - launches0
-        ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
-        del flush
-    else:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        launches = hr.kernel_launches(local) - launches0
-        ms = e0.elapsed_time(e1) / args.steps
+    ms, per = timed_steps(args.steps)
+    launches = hr.kernel_launches(local) - launches0
     if dist:
         dist.barrier()
+    # ---- distribution: >= 50 replays and >= 1 s of load, each step bracketed by its own events
+    # (their spread; the nvidia-smi clock samples cover this stretch too) ----
+    n_rep = max(50, int(1.0 / max(ms / 1e3, 1e-6)) + 1)
+    t_rep0 = time.perf_counter()
+    if flush is not None:
+        _, reps = timed_steps(n_rep)
+    else:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n_rep + 1)]
+        evs[0].record(stream)
+        for i in range(n_rep):
+            step()
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        reps = [evs[i].elapsed_time(evs[i + 1]) for i in range(n_rep)]
+    rep_span = time.perf_counter() - t_rep0
     clk = clocks.stop()
-    # ---- kernel durations (roofline): CUDA events on the launching stream around the same
-    # calls, in an instrumented pass of the same workload right after the timed one ----
+    timing = {"replays": n_rep, "median_ms": round(pct(reps, 50), 4), "p10_ms": round(pct(reps, 10), 4),
+              "p90_ms": round(pct(reps, 90), 4), "span_s": round(rep_span, 2),
+              "how": ("each replay: 256 MB L2 flush, then events around one step" if flush is not None else
+                      "back-to-back steps, an event between consecutive steps")}
+    if per is not None:
+        timing["timed_region_per_step_ms"] = [round(v, 4) for v in per]
+
+    # ---- in-step kernel durations of the timed schedule (globaltimer step trace) ----
+    in_step = trace_step(hr, step, local, B, H, W, dev)
+    path = hr.last_path(local)  # 0 separate kernels, 3 grouped step
+    groups_used = hr.get_policy("groups", local)
+    # ---- informational: the separate-kernel schedule's stages, CUDA events between kernels ----
+    hr.set_policy("groups", 0, local)
+    for _ in range(3):
+        step()
     hr.profile_enable(local, True)
     hr.profile_collect(local)
-    for _ in range(min(args.steps, 20)):
+    for _ in range(min(max(args.steps, 5), 20)):
+        if flush is not None:
+            flush.fill_(1)
         step()
-    (st0, st1, st2), nsteps = hr.profile_collect(local)
+    (h_ms, s_ms, a_ms), n2 = hr.profile_collect(local)
     hr.profile_enable(local, False)
-    st0, st1, st2 = (v / max(nsteps, 1) for v in (st0, st1, st2))
-    path = hr.last_path(local)  # 0 separate kernels, 1 fused, 2 chunk pipeline
-    fused, chunked = path == 1, path in (2, 3)
-    # informational: the separate-kernel stage split of the same workload (not the timed path)
-    split = None
-    if fused or chunked:
-        groups_used = hr.get_policy("groups", local)
-        hr.set_policy("fused_min_b", 0, local)
-        hr.set_policy("chunks", 1, local)
-        hr.set_policy("groups", 0, local)
-        for _ in range(3):
-            step()
-        hr.profile_enable(local, True)
-        hr.profile_collect(local)
-        for _ in range(min(args.steps, 20)):
-            step()
-        (h_ms, s_ms, a_ms), n2 = hr.profile_collect(local)
-        hr.profile_enable(local, False)
-        hr.set_policy("fused_min_b", int(os.environ.get("HR_FUSED_MIN_B", "0")), local)
-        hr.set_policy("chunks", max(1, int(os.environ.get("HR_CHUNKS", "1"))), local)
-        hr.set_policy("groups", groups_used, local)
-        split = (h_ms / max(n2, 1), s_ms / max(n2, 1), a_ms / max(n2, 1))
-    else:
-        split = (st0, st1, st2)
-    hist_ms, solve_ms, apply_ms = split
+    hr.set_policy("groups", groups_used, local)
+    hist_ms, solve_ms, apply_ms = (v / max(n2, 1) for v in (h_ms, s_ms, a_ms))
     ms = max_over_ranks(ms, dist, dev)
 
     # ---- end to end through the C-ABI with host buffers (H2D + enhance + D2H per step) ----
@@ -360,6 +471,7 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize(dev)
         if dist:
             dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         ne = max(3, min(args.steps, 10))
         for _ in range(ne):
@@ -374,34 +486,21 @@ def run_ours(args, world, rank, local):
                "note": f"hr_enhance_host: pinned host in/out, H2D | enhance | D2H pipelined over "
                        f"{min(args.e2e_chunks or 8, B)} image chunks"}
 
-    if fused:
-        path_name = "fused persistent kernel (hist -> per-image solve + LUT -> apply)"
-    elif path == 3:
+    if path == 3:
         ng = groups_used if groups_used >= 2 else 2  # -1 = auto: 2 groups
         path_name = (f"grouped step ({ng} image groups: hist(k+1) beside solve(k), apply beside the "
                      "last group's solves)")
-    elif chunked:
-        path_name = "stream pipeline over image chunks"
     else:
         path_name = "separate kernels (hist | solve + LUT | apply)"
     value = aggregate_mps(world, B, H, W, ms)
     peak, peak_src = peaks()
-    e2e_frac = BYTES_PER_PX * (B * H * W) / (ms / 1e3) / 1e9 / peak
-    # dominant kernel (HBM-bound).  Fused: the one k_fused launch per step, algorithmic bytes
-    # 9 per pixel (RGB read by the histograms, read again and written by the apply).
-    # Separate kernels: the larger of the two streaming kernels.
-    if fused:
-        name, kms, kbytes = "k_fused", st1, BYTES_PER_PX * B * H * W
-    else:
-        kern = {"k_hist": (hist_ms, 3 * B * H * W), "k_apply": (apply_ms, 6 * B * H * W)}
-        name = max(kern, key=lambda k: kern[k][0])
-        kms, kbytes = kern[name]
-    achieved = kbytes / (kms / 1e3) / 1e9
+    step_bytes = BYTES_PER_PX * B * H * W
+    achieved = step_bytes / (ms / 1e3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(args.config, {}).get(name)
+            traffic = json.load(open(tf)).get(args.config, {}).get("step")
         except Exception:
             traffic = None
 
@@ -409,9 +508,14 @@ def run_ours(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
 
-        v, cores, sample = oracle_sample(args.config, x_pin.numpy(),
-                                         oracle.Params(use_epsilon=cfg.use_epsilon))
-        cpu_base = {"value": round(v, 3), "unit": "MP/s", "cores": cores, "kind": "oracle", "sample": sample}
+        po = oracle.Params(use_epsilon=cfg.use_epsilon)
+        v, cores, sample = oracle_sample(args.config, x_pin.numpy(), po)
+        cpu_base = {"value": round(v, 3), "unit": "MP/s", "cores": cores, "kind": "oracle", "sample": sample,
+                    "cpu_model": cpu_model(), "host_threads": cpu_cores()}
+        if B > 1:  # the batched configs: the same oracle on one core too
+            v1, c1, s1 = oracle_sample(args.config, x_pin.numpy(), po, budget_s=6.0, max_threads=1)
+            cpu_base["one_core"] = {"value": round(v1, 3), "unit": "MP/s", "cores": c1, "sample": s1}
+        cpu_base["stages"] = oracle_stages(x_pin.numpy(), po)
 
     if rank == 0:
         line = {
@@ -420,17 +524,21 @@ def run_ours(args, world, rank, local):
             "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8+f64", "data": "synthetic",
             "config": config_dict(args.config, world, params),
-            "hbm_roofline_frac_e2e": round(e2e_frac, 4),
-            "roofline": {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "peak_source": peak_src, "algorithmic_bytes_per_launch": kbytes},
+            "hbm_roofline_frac_e2e": round(achieved / peak, 4),
+            # the unit launched per step is hr_enhance (its kernels overlap in the grouped step):
+            # 9 algorithmic bytes per pixel over the timed step
+            "roofline": {"bound": "hbm", "kernel": "hr_enhance step (" + path_name + ")",
+                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": step_bytes},
             "path": path_name,
-            "fused_ms": {"zero": round(st0, 4), "k_fused": round(st1, 4)} if fused else None,
-            "stages_ms" if not (fused or chunked) else "stages_ms_unfused_info":
-                         {"hist": round(hist_ms, 4), "solve": round(solve_ms, 4), "apply": round(apply_ms, 4),
-                          "hist_GBs": round(3 * B * H * W / (hist_ms / 1e3) / 1e9, 1),
-                          "apply_GBs": round(6 * B * H * W / (apply_ms / 1e3) / 1e9, 1),
-                          "solve_us_per_image": round(solve_ms * 1e3 / B, 3)},
+            "timing": timing,
+            "in_step": in_step,
+            "stages_ms_separate_kernels_info":
+                {"hist": round(hist_ms, 4), "solve": round(solve_ms, 4), "apply": round(apply_ms, 4),
+                 "hist_GBs": round(3 * B * H * W / (hist_ms / 1e3) / 1e9, 1),
+                 "apply_GBs": round(6 * B * H * W / (apply_ms / 1e3) / 1e9, 1),
+                 "note": "policy groups=0, CUDA events between kernels (informational, not the timed schedule)"},
             "cpu_baseline": cpu_base,
             "e2e": e2e,
             "clocks": clk,

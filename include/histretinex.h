@@ -144,19 +144,15 @@ hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_de
                    int32_t H, int32_t W, uint8_t* rgb_out_dev, void* stream);
 
 /* Steps (1)-(4) for the whole batch ("matching its histogram with the one provided by
-   HistRetinex") on `stream`.  Default: the histogram, solve + LUT and apply kernels in order,
-   chained by programmatic dependent launch, the apply acquiring each image's LUT-ready flag
-   (so it overlaps the solver's tail); for B >= 2 the grouped step (two image groups, policy
-   "groups": the second group's histograms run beside the first group's solves, the apply
-   beside the second group's solves).  Policy (hr_set_policy): for fused_min_b <= B <=
-   fused_max_b (fused_min_b = 0 = off by default) with 16-byte aligned buffers and
-   H*W % 16 == 0, ONE persistent kernel runs the
-   histograms, each image's solve + LUT as soon as its histograms are complete, and the
-   apply (solves overlap the streaming passes); otherwise the histogram, solve + LUT and
-   apply kernels run in order (or as a chunk pipeline when chunks > 1).  Every policy gives
-   bit-identical outputs.  While stage profiling is enabled the separate kernels are used.
-   Optional debug outputs (device, nullable): hist_s [B][256], lut [B][256], iters [B].
-   rgb_out must not alias rgb_in.  Workspace: hr_workspace_bytes(B,H,W), device. */
+   HistRetinex") on `stream`.  One image (or policy groups = 0): the histogram, solve + LUT and
+   apply kernels in order, chained by programmatic dependent launch, the apply acquiring each
+   image's LUT-ready flag (so it overlaps the solver's tail).  B >= 2: the grouped step (two
+   image groups, policy "groups": the second group's histograms run beside the first group's
+   solves, the apply beside the second group's solves).  Every policy gives bit-identical
+   outputs.  The first call with a new gamma builds its index_1 table (Eqs. 17-19) and waits for
+   it (host-blocking, once per gamma per context).  Optional debug outputs (device, nullable):
+   hist_s [B][256], lut [B][256], iters [B] (hr_enhance_debug).  rgb_out must not alias rgb_in.
+   Workspace: hr_workspace_bytes(B,H,W), device. */
 hr_status hr_enhance(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H, int32_t W,
                      const hr_params* params, uint8_t* rgb_out_dev, void* ws_dev, void* stream);
 
@@ -206,67 +202,49 @@ hr_status hr_quality(hr_ctx* ctx, const uint8_t* a_dev, const uint8_t* b_dev, in
 /* Stage timing (measurement only).  While enabled, every hr_enhance records four CUDA
    events on its stream.  Separate-kernel path: before the histogram kernel, after it,
    after the solver + LUT, after the apply kernel -> stage_ms[0] histogram incl. its
-   memsets, [1] solve + LUT, [2] apply.  Fused path: before the accumulator memset, before
-   the fused kernel, after it (twice) -> stage_ms[0] memset, [1] the fused kernel, [2] 0.
-   Chunk pipeline (chunks > 1): stage_ms = [0, 0, whole pipeline].
+   zeroing, [1] solve + LUT, [2] apply.
    hr_profile_collect waits for the recorded events, returns the summed milliseconds over
-   the *steps calls since the last collect, and resets the counters.  At most 4096 calls
+   the *steps calls since the last collect, and resets the counters.  Grouped step: before the
+   accumulator zeroing, after it, after the last solver launch, after the apply -> stage_ms[0]
+   zeroing, [1] histograms + solves of all groups, [2] the apply (stages overlap on the device,
+   so only the sum is a step time).  At most 4096 calls
    are kept between collects (HR_EINVAL beyond). */
 hr_status hr_profile_enable(hr_ctx* ctx, int32_t on);
 hr_status hr_profile_collect(hr_ctx* ctx, double* stage_ms, int32_t* steps);
 
+/* Step timeline (measurement only).  Binds a device record buffer for every later launch on
+   this context's device (NULL records unbinds; count and capacity are then ignored): thread 0
+   of each CTA of the histogram, solver and apply kernels appends one 48-byte record
+     { uint32 kind (1 histogram, 3 solver, 4 apply), cta, sm, aux;
+       uint64 start_ns, mid_ns, end_ns, pad }
+   at records[atomicAdd(count, 1)] while that index is below capacity (%globaltimer
+   nanoseconds; aux = (hist_s address of the launch's first image) >> 8 for the histogram and
+   solver kernels, so launches of one step are told apart; mid_ns = when a solver CTA's image
+   histograms were complete).  The caller zeroes *count (device uint32) and owns both buffers.
+   Outputs of every entry point are unchanged while bound. */
+hr_status hr_trace_bind(hr_ctx* ctx, void* records_dev, uint32_t* count_dev, uint32_t capacity);
+
 /* Execution policy of hr_enhance (performance only: results never depend on it).  Keys:
-     "fused_min_b"  persistent fused kernel for B >= value (0: never)        default 0
-     "fused_max_b"  ... and B <= value (0: auto = #SMs / 2)                  default 0
-     "fused_cpsm"   fused-kernel CTAs per SM (1..2)                           default 2
-     "fused_bands"  histogram band work items per CTA (1..2^20)            default 2
-     "fused_gs"     1024-pixel chunks per apply work ticket (1..2^30)        default 8
-     "chunks"       unfused path: image chunks of the stream pipeline (>= 1)  default 1
-     "hist_cpsm", "apply_cpsm"  unfused kernels' CTAs per SM (1..2)         default 2
-     "warp_solver"  unfused path: warp-per-image solver for small supports   default 0
-     "solve_cpsm"   solver CTAs per SM: 1, 2, 0 = auto (1 when B <= #SMs)   default 0
-     "apply_dyn"    separate kernels: 1 = the apply takes images in the order     default 0
-                    their LUTs complete (completion queue filled by the solver);
-                    2 = natural order after the solver grid; both with per-warp
-                    tickets of apply_gs chunks that balance the streaming work;
-                    3 = first half of the images split statically, second half
-                    by CTA tickets, gated by the per-image LUT-ready flags
-     "apply_gs"     1024-pixel chunks per dynamic-apply warp ticket (>= 1)      default 8
-     "hist_overlap" separate kernels: each solver CTA starts when its image's  default 0
-                    histogram segments are flushed (histograms at 2x256 threads per SM)
+     "hist_cpsm", "apply_cpsm"  streaming kernels' CTAs per SM (1..2)          default 2
+     "solve_cpsm"   solver CTAs per SM: 1, 2, 0 = auto (1 when B <= #SMs)      default 0
+     "solve_wide_px" one solver CTA per SM (B <= #SMs): 512-thread CTAs for     default 4194304
+                    images of H*W >= value pixels (0: never; large images have
+                    large supports: C4 103 vs 121 us per image, while small
+                    supports are faster at 256 threads: C2 37 vs 43 us)
      "groups"       grouped step (>= 2): images in G groups, launched in order  default -1
                     hist(0) solve(0) hist(1) solve(1) ... solve(G-1) apply; the
                     histograms of group k+1 run beside the solves of group k (they
                     do not wait for them), the apply (every CTA: groups 0..G-2
-                    first) beside the last group's solves; streaming grids sized
-                    to the slots the resident solver CTAs leave.  0/1: off;
-                    -1: auto = 2 when B >= 2
+                    first, the last group by CTA tickets) beside the last group's
+                    solves; streaming grids sized to the slots the resident solver
+                    CTAs leave.  0/1: off (separate kernels); -1: auto = 2 when B >= 2
      "group_first_pct" grouped step with 2 groups: the first group's share of  default -1
-                    the batch in % (0: half; -1: auto = 38 for B <= #SMs / 2, a short
-                    first histogram pass hiding the first solves under the second,
-                    C3 0.254 vs 0.261 ms; 90 for larger batches, the last group's
-                    few solves beside the first group's apply, C5 0.167 vs 0.177)
-     "group_apply"  grouped step's apply: 0 static shares (groups 0..G-2, then     default 2
-                    the last group); 1 the last group by CTA tickets through a
-                    shared-memory ring (k_apply_dyn); 2 the last group by CTA tickets
-                    of 8 * apply_gs chunks taken at CTA barriers (k_apply_tma)
-     "apply_tail_pct" grouped step with group_apply 2: % of the first groups'    default 0
-                    chunks also taken by tickets (measured no gain)
-     "solve_queue"  grouped step: each solver CTA takes the next image in the     default 0
-                    order the histograms complete (a queue k_hist fills) instead of
-                    its own image (measured no gain: the apply still goes in image order)
-     "solve_wide_px" hr_enhance, one solver CTA per SM (B <= #SMs): 512-thread   default 4194304
-                    solver CTAs for images of H*W >= value pixels (0: never; large
-                    images have large supports: C4 103 vs 121 us per image, while
-                    small supports are faster at 256 threads: C2 37 vs 43 us)
-     "solve_waves"  separate kernels, B > #SMs: one solver CTA per SM solving    default 0
-                    its images in turn, the apply beside it (off: the solver and
-                    apply CTAs do not share SMs; C5 0.203-0.261 vs 0.175 ms)
-     "solve_waves_ag" apply CTAs per SM launched with solve_waves (1..2)         default 1
-     "hist_tma"     histogram kernel with TMA-staged rows (one CTA per SM; in     default 0
-                    the hist_overlap form 512 threads in image waves) for 16-B
-                    aligned batches with W % 16 == 0 (256 <= W <= 8192) or
-                    W % 16 == 8 (128 <= W <= 4096, B*H*W*3 % 16 == 0)
+                    the batch in % (0: equal groups; -1: auto = 38 for B <= #SMs / 2,
+                    a short first histogram pass hiding the first solves under the
+                    second, C3 0.254 vs 0.261 ms; 90 for larger batches, the last
+                    group's few solves beside the first group's apply, C5 0.167 vs 0.177)
+     "apply_gs"     grouped step's apply: 1024-pixel chunks per warp in one CTA  default 8
+                    ticket of the last group (>= 1)
    The environment variables HR_<KEY upper-cased> set the initial values at hr_create.
    Returns HR_EINVAL for an unknown key or an out-of-range value (nothing changes). */
 hr_status hr_set_policy(hr_ctx* ctx, const char* key, int64_t value);
@@ -279,8 +257,7 @@ hr_status hr_get_policy(hr_ctx* ctx, const char* key, int64_t* value);
 int64_t hr_kernel_launches(const hr_ctx* ctx);
 
 /* Execution path of the last hr_enhance on this context: 0 separate kernels (histogram |
-   solve + LUT | apply), 1 the persistent fused kernel, 2 the chunk pipeline, 3 the grouped
-   step (policy "groups"); -1 none yet or a NULL ctx. */
+   solve + LUT | apply), 3 the grouped step (policy "groups"); -1 none yet or a NULL ctx. */
 int32_t hr_last_path(const hr_ctx* ctx);
 
 #ifdef __cplusplus

@@ -24,7 +24,7 @@ from ._lib import HrError
 __all__ = ["Params", "HrError", "hr_histogram", "hr_solve", "hr_match", "hr_apply", "hr_enhance",
            "hr_enhance_debug", "workspace_bytes", "version", "profile_enable", "profile_collect",
            "set_policy", "kernel_launches", "hr_enhance_host", "last_path", "hr_solve_trace", "hr_he",
-           "hr_quality"]
+           "hr_quality", "trace_bind"]
 
 
 @dataclass
@@ -78,6 +78,33 @@ def _cuda(t: torch.Tensor, dtype: torch.dtype, name: str) -> torch.Tensor:
     return t
 
 
+def _buf(t: torch.Tensor, dtype: torch.dtype, shape, device: torch.device, name: str) -> torch.Tensor:
+    """A caller-supplied buffer the C side will write or read: the C-ABI cannot check sizes, so
+    dtype, device, contiguity and the exact shape are checked here."""
+    _cuda(t, dtype, name)
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t
+
+
+def _ws_check(ws: torch.Tensor, nbytes: int, device: torch.device, name: str = "workspace") -> torch.Tensor:
+    _cuda(ws, torch.uint8, name)
+    if ws.device != device:
+        raise ValueError(f"{name} is on {ws.device}, expected {device}")
+    if ws.numel() < nbytes:
+        raise ValueError(f"{name} has {ws.numel()} bytes, needs {nbytes}")
+    return ws
+
+
+def _hist_pair(hist_s: torch.Tensor, hist_g: torch.Tensor):
+    _cuda(hist_s, torch.int32, "hist_s")
+    if hist_s.dim() != 2 or hist_s.shape[1] != 256:
+        raise ValueError("hist_s must be int32 [B, 256]")
+    _buf(hist_g, torch.int32, hist_s.shape, hist_s.device, "hist_g")
+
+
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
@@ -126,8 +153,7 @@ def hr_histogram(rgb: torch.Tensor, grad_norm: int = 0):
 def hr_solve(hist_s: torch.Tensor, hist_g: torch.Tensor, params: Params | None = None):
     """(2) Algorithm 1 + Eqs. 17-20.  Returns (hL, hR, target) float64 [B,256] and iters int32 [B]."""
     p = params or Params()
-    _cuda(hist_s, torch.int32, "hist_s")
-    _cuda(hist_g, torch.int32, "hist_g")
+    _hist_pair(hist_s, hist_g)
     B = hist_s.shape[0]
     dev = hist_s.device
     hL = torch.empty((B, 256), dtype=torch.float64, device=dev)
@@ -146,8 +172,7 @@ def hr_solve_trace(hist_s: torch.Tensor, hist_g: torch.Tensor, params: Params | 
     """hr_solve plus the Eq. 10 objective trace (3 values per update, K frozen).  Returns
     (hL, hR, target, iters, trace) with trace float64 [B, 3 * max_iter]."""
     p = params or Params()
-    _cuda(hist_s, torch.int32, "hist_s")
-    _cuda(hist_g, torch.int32, "hist_g")
+    _hist_pair(hist_s, hist_g)
     B = hist_s.shape[0]
     dev = hist_s.device
     hL = torch.empty((B, 256), dtype=torch.float64, device=dev)
@@ -167,9 +192,11 @@ def hr_solve_trace(hist_s: torch.Tensor, hist_g: torch.Tensor, params: Params | 
 def hr_match(hist_s: torch.Tensor, target: torch.Tensor):
     """(3) CDF + LUT.  Returns (lut uint8 [B,256], status int32 [B])."""
     _cuda(hist_s, torch.int32, "hist_s")
-    _cuda(target, torch.float64, "target")
+    if hist_s.dim() != 2 or hist_s.shape[1] != 256:
+        raise ValueError("hist_s must be int32 [B, 256]")
     B = hist_s.shape[0]
     dev = hist_s.device
+    _buf(target, torch.float64, (B, 256), dev, "target")
     lut = torch.empty((B, 256), dtype=torch.uint8, device=dev)
     stt = torch.empty((B,), dtype=torch.int32, device=dev)
     ctx = _context(dev)
@@ -181,9 +208,8 @@ def hr_apply(rgb: torch.Tensor, lut: torch.Tensor, out: torch.Tensor | None = No
     """(4) per-pixel LUT + colour reconstruction."""
     x = _images(rgb)
     B, H, W, _ = x.shape
-    _cuda(lut, torch.uint8, "lut")
-    if out is None:
-        out = torch.empty_like(x)
+    _buf(lut, torch.uint8, (B, 256), x.device, "lut")
+    out = torch.empty_like(x) if out is None else _buf(out, torch.uint8, x.shape, x.device, "out")
     ctx = _context(x.device)
     _check(_lib.load().hr_apply(ctx, _ptr(x), _ptr(lut), B, H, W, _ptr(out), _stream(x.device)), ctx)
     return out
@@ -195,14 +221,29 @@ def hr_enhance(rgb: torch.Tensor, params: Params | None = None, out: torch.Tenso
     p = params or Params()
     x = _images(rgb)
     B, H, W, _ = x.shape
-    if out is None:
-        out = torch.empty_like(x)
-    ws = workspace if workspace is not None else _workspace(B, H, W, x.device)
+    out = torch.empty_like(x) if out is None else _buf(out, torch.uint8, x.shape, x.device, "out")
+    if x.numel() and out.data_ptr() == x.data_ptr():
+        raise ValueError("out must not alias rgb")
+    ws = (_ws_check(workspace, workspace_bytes(B, H, W), x.device) if workspace is not None
+          else _workspace(B, H, W, x.device))
     pc = p.c()
     ctx = _context(x.device)
     _check(_lib.load().hr_enhance(ctx, _ptr(x), B, H, W, ctypes.byref(pc), _ptr(out), _ptr(ws),
                                   _stream(x.device)), ctx)
     return out
+
+
+def trace_bind(records: torch.Tensor | None, count: torch.Tensor | None, capacity: int, device=None) -> None:
+    """hr_trace_bind (measurement): bind a device record buffer (48-byte records) and a uint32
+    counter for the step timeline of later launches on `device`; records=None unbinds."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    ctx = _context(dev)
+    if records is not None:
+        _cuda(records, torch.uint8, "records")
+        _cuda(count, torch.int32, "count")
+        if records.numel() < 48 * capacity:
+            raise ValueError("records holds fewer than capacity records")
+    _check(_lib.load().hr_trace_bind(ctx, _ptr(records), _ptr(count), int(capacity)), ctx)
 
 
 def profile_enable(device=None, on: bool = True) -> None:
@@ -254,9 +295,14 @@ def hr_enhance_host(rgb_host: torch.Tensor, params: Params | None = None, out_ho
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     if out_host is None:
         out_host = torch.empty_like(x, pin_memory=x.is_pinned())
-    in_dev = torch.empty(x.shape, dtype=torch.uint8, device=dev) if in_dev is None else in_dev
-    out_dev = torch.empty(x.shape, dtype=torch.uint8, device=dev) if out_dev is None else out_dev
-    ws = _workspace(B, H, W, dev) if workspace is None else workspace
+    elif (out_host.device.type != "cpu" or out_host.dtype != torch.uint8 or tuple(out_host.shape) != tuple(x.shape)
+          or not out_host.is_contiguous()):
+        raise ValueError(f"out_host must be a contiguous CPU uint8 tensor of shape {tuple(x.shape)}")
+    in_dev = (torch.empty(x.shape, dtype=torch.uint8, device=dev) if in_dev is None
+              else _buf(in_dev, torch.uint8, x.shape, dev, "in_dev"))
+    out_dev = (torch.empty(x.shape, dtype=torch.uint8, device=dev) if out_dev is None
+               else _buf(out_dev, torch.uint8, x.shape, dev, "out_dev"))
+    ws = _workspace(B, H, W, dev) if workspace is None else _ws_check(workspace, workspace_bytes(B, H, W), dev)
     pc = (params or Params()).c()
     ctx = _context(dev)
     _check(_lib.load().hr_enhance_host(ctx, _ptr(x), B, H, W, ctypes.byref(pc), _ptr(out_host), _ptr(in_dev),
@@ -267,7 +313,7 @@ def hr_enhance_host(rgb_host: torch.Tensor, params: Params | None = None, out_ho
 
 
 def last_path(device=None) -> int:
-    """hr_last_path: 0 separate kernels, 1 fused kernel, 2 chunk pipeline (last hr_enhance)."""
+    """hr_last_path: 0 separate kernels, 3 grouped step (last hr_enhance)."""
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     return int(_lib.load().hr_last_path(_context(dev)))
 
@@ -277,7 +323,7 @@ def hr_he(rgb: torch.Tensor, out: torch.Tensor | None = None, return_lut: bool =
     x = _images(rgb)
     B, H, W, _ = x.shape
     dev = x.device
-    out = torch.empty_like(x) if out is None else out
+    out = torch.empty_like(x) if out is None else _buf(out, torch.uint8, x.shape, dev, "out")
     lut = torch.empty((B, 256), dtype=torch.uint8, device=dev)
     ws = _workspace(B, H, W, dev)
     ctx = _context(dev)

@@ -6,7 +6,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SOURCES = ["csrc/hr_api.cu", "csrc/k_hist.cu", "csrc/k_solve.cu", "csrc/k_solve_warp.cu", "csrc/k_apply.cu", "csrc/k_fused.cu", "csrc/k_quality.cu"]
+SOURCES = ["csrc/hr_api.cu", "csrc/k_hist.cu", "csrc/k_solve.cu", "csrc/k_apply.cu", "csrc/k_quality.cu"]
 HEADERS = ["../include/histretinex.h"]  # + every csrc/*.cuh (see stale())
 LIB = os.path.join(HERE, "libhistretinex.so")
 NVCC_FLAGS = [

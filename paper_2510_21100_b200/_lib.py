@@ -20,7 +20,7 @@ EXPORTS = (
     "hr_version", "hr_workspace_bytes", "hr_histogram", "hr_solve", "hr_match", "hr_apply",
     "hr_enhance", "hr_enhance_debug", "hr_profile_enable", "hr_profile_collect", "hr_set_policy",
     "hr_kernel_launches", "hr_enhance_host", "hr_last_path", "hr_solve_trace", "hr_he",
-    "hr_quality_workspace_bytes", "hr_quality", "hr_get_policy",
+    "hr_quality_workspace_bytes", "hr_quality", "hr_get_policy", "hr_trace_bind",
 )
 
 
@@ -87,6 +87,7 @@ def load() -> ctypes.CDLL:
         "hr_he": ([vp, vp, i64, i32, i32, vp, vp, vp, vp], i32),
         "hr_quality_workspace_bytes": ([i64, i32, i32], sz),
         "hr_quality": ([vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp], i32),
+        "hr_trace_bind": ([vp, vp, vp, ctypes.c_uint32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

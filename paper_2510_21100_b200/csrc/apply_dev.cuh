@@ -1,6 +1,5 @@
 // apply_dev.cuh -- device helpers of kernel (d): the exact integer colour reconstruction and
-// the TMA bulk-copy / mbarrier PTX wrappers.  Shared by k_apply (k_apply.cu) and the persistent
-// fused kernel (k_fused.cu).
+// the TMA bulk-copy / mbarrier PTX wrappers, used by k_apply (k_apply.cu).
 //
 // P:308 ("we utilize the histogram matching to estimate the enhanced image") and P:59
 // (S is the HSV value channel): V = max(R,G,B), V' = LUT[V]; replacing V in hexcone HSV
@@ -82,16 +81,6 @@ __device__ __forceinline__ void build_tab(uint2* tab, const uint8_t* __restrict_
 #pragma unroll
   for (int v = lane; v < kLevels; v += 32) tab[v] = make_uint2(ab_of(v, __ldcg(lut_b + v)), __ldg(&g_magic.m[v]));
 }
-// the same from LUT bytes [8 lane, 8 lane + 8) already in registers (lo: bytes 0-3, hi: 4-7)
-__device__ __forceinline__ void build_tab_regs(uint2* tab, uint2 lut8, int lane) {
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const int v = 8 * lane + m;
-    const uint32_t L = (m < 4 ? lut8.x >> (8 * m) : lut8.y >> (8 * (m - 4))) & 0xFFu;
-    tab[v] = make_uint2(ab_of(v, L), __ldg(&g_magic.m[v]));
-  }
-}
-
 // ---- PTX wrappers: mbarrier + bulk async copies (sm_90+, used on sm_100a) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

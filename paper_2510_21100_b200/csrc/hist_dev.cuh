@@ -1,6 +1,5 @@
 // hist_dev.cuh -- device body of kernel (a): fused colour convert + gradient + privatised
-// histograms over one image segment.  Shared by k_hist (k_hist.cu) and the persistent fused
-// kernel (k_fused.cu).
+// histograms over one image segment, launched by k_hist (k_hist.cu).
 //
 // PAPER.md Alg. 1 lines "Compute the histogram of the low-light image H_C(S)" and
 // "Compute the histogram of the gradient image H_C(grad S)", Eq. 3.

@@ -1,7 +1,6 @@
 // k_apply.cu -- kernel (d): streaming LUT application + colour reconstruction.
 //
-// Standalone launch of the LUT application (hr_apply, serial / chunk-pipelined hr_enhance);
-// the helpers are in apply_dev.cuh.
+// The LUT application of hr_apply and hr_enhance; the helpers are in apply_dev.cuh.
 // P:308 ("we utilize the histogram matching to estimate the enhanced image") and P:59
 // (S is the HSV value channel): V = max(R,G,B), V' = LUT[V]; replacing V in hexcone HSV
 // scales every channel by V'/V (reading R17), rounded half up:
@@ -28,7 +27,7 @@ namespace {
 __global__ void __launch_bounds__(kApplyThreads, 2)
 k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int64_t B, int64_t HW,
             uint8_t* __restrict__ out, const uint32_t* __restrict__ ready, int64_t b_last,
-            uint32_t* __restrict__ ticket, uint32_t GS, uint32_t tail_pct) {
+            uint32_t* __restrict__ ticket, uint32_t GS) {
   extern __shared__ __align__(128) unsigned char smraw[];
   ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
   __shared__ uint32_t tk_s;
@@ -51,9 +50,7 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   if (b_last <= 0 || b_last > B) b_last = B;
   const uint32_t GA0 = (uint32_t)(b_last * (int64_t)cpi), GB0 = (uint32_t)(B * (int64_t)cpi) - GA0;  // < 2^31
   const bool dynB = ticket != nullptr && GB0 > 0;
-  // with tickets, the last tail_pct % of part A joins the ticketed part (natural order)
-  const uint32_t GA = dynB ? GA0 - (uint32_t)((uint64_t)GA0 * min(tail_pct, 100u) / 100u) : GA0;
-  const uint32_t GB = GA0 + GB0 - GA;
+  const uint32_t GA = GA0, GB = GB0;
   const uint32_t a0 = (uint32_t)((uint64_t)GA * blockIdx.x / gridDim.x), a1 = (uint32_t)((uint64_t)GA * (blockIdx.x + 1) / gridDim.x);
   const uint32_t c0 = GA + (dynB ? 0u : (uint32_t)((uint64_t)GB * blockIdx.x / gridDim.x));
   const uint32_t c1 = GA + (dynB ? 0u : (uint32_t)((uint64_t)GB * (blockIdx.x + 1) / gridDim.x));
@@ -91,8 +88,7 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
       where(chunk(i), off, bytes, b);
       if ((int64_t)b != cur_img) {  // per-warp LUT table for this image
         __syncwarp();
-        if (ready && lane == 0)
-          while (ld_acquire(ready + b) == 0u) __nanosleep(100);
+        if (ready && lane == 0) wait_flag_geq(ready + b, 1u, 100);
         __syncwarp();
         build_tab(tab, lut + (uint64_t)b * kLevels, lane);
         __syncwarp();
@@ -142,233 +138,6 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   TRACE_END(4u, 0u, 0ull);
 }
 
-// ---------------------------------------------------------------- dynamic (ticketed) apply
-// The same per-warp TMA pipeline, fed by tickets over (image position, group of GS chunks),
-// each warp's next ticket fetched while it works on the current one.  With a completion queue
-// the loader lane acquires queue[pos] (k_solve released it after writing that image's LUT), so
-// warps always work on images whose LUT is done and the apply starts with the first finished
-// solve; without one (queue == NULL) images go in natural order after the whole solver grid
-// (griddepcontrol.wait) -- the tickets then only balance the streaming work across warps
-// whatever their start times (CTAs that become resident late take fewer tickets).  Each new image's LUT is loaded into registers when its first chunk is issued
-// (kAhead chunks before it is computed).  Deadlock-free: launched (PDL) only once every solver
-// CTA is resident, and each solve fills one queue slot.
-struct DynSmem {
-  static constexpr int kRing = 4;
-  uint2 meta[kWarps][kStages];
-  uint32_t ring_t[kRing];
-  int ring_tag[kRing], ring_read[kWarps], ring_claim;
-};
-
-__global__ void __launch_bounds__(kApplyThreads, 2)
-k_apply_dyn(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int64_t B, int64_t HW,
-            uint8_t* __restrict__ out, const uint32_t* __restrict__ queue, uint32_t* __restrict__ ticket, uint32_t GS,
-            const uint32_t* __restrict__ ready, int64_t b_last) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  ApplySmem& s = *reinterpret_cast<ApplySmem*>(smraw);
-  // all shared memory is dynamic: a static block before it would push the 128-B aligned
-  // dynamic block to the next 1 KB and leave room for only one CTA per SM
-  DynSmem& x = *reinterpret_cast<DynSmem*>(smraw + sizeof(ApplySmem));
-  auto& meta = x.meta;  // (image, chunk) of each stage, image = kEndImg: end
-  constexpr uint32_t kEndImg = 0xFFFFFFFFu;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  TRACE_T0();
-  // with the completion queue there is no grid-wide wait: LUTs arrive through the queue; with
-  // per-image ready flags (natural order) each image's LUT is acquired before its first group;
-  // with neither every LUT is read after the solver grid has completed
-  if (!queue && !ready) pdl_wait();
-  pdl_trigger();
-  if (lane == 0) {
-    for (int k = 0; k < kStages; ++k) mbar_init(&s.bar[w][k], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const uint32_t cpi = (uint32_t)((HW + kChunkPx - 1) / kChunkPx);
-  const uint32_t gpi = (cpi + GS - 1) / GS;
-  // hybrid form (0 < b_last < B, natural order with ready flags): images [0, b_last) are split
-  // statically (this CTA's contiguous share, its warps interleaved chunk by chunk, as in
-  // k_apply_tma) and only images [b_last, B) go by tickets, so CTAs that became resident late
-  // or run slower take fewer of them
-  if (queue || b_last <= 0 || b_last > B) b_last = 0;
-  const uint32_t GA = (uint32_t)(b_last * (int64_t)cpi);
-  const uint32_t a0 = (uint32_t)((uint64_t)GA * blockIdx.x / gridDim.x), a1 = (uint32_t)((uint64_t)GA * (blockIdx.x + 1) / gridDim.x);
-  const uint32_t nA = (a1 - a0 > (uint32_t)w) ? (a1 - a0 - w + kWarps - 1) / kWarps : 0u;
-  uint32_t sA = 0;  // static chunks issued so far
-  const uint64_t ngroups = (uint64_t)(B - b_last) * gpi;
-  // hybrid form, part B: CTA tickets of kWarps * GS contiguous chunks (all warps of the CTA
-  // stream one ticket together, warp w taking chunks w, w + kWarps, ... as in the static part:
-  // per-warp tickets scatter the DRAM streams and measured far slower).  The CTA's k-th ticket
-  // is fetched by the first warp that needs it and published in a ring of kRing slots; a slot
-  // is refilled only after every warp has read its previous ticket (no lag limit otherwise).
-  constexpr int kRing = DynSmem::kRing;
-  uint32_t* ring_t = x.ring_t;
-  int *ring_tag = x.ring_tag, *ring_read = x.ring_read;
-  int& ring_claim = x.ring_claim;
-  const uint32_t GB = (uint32_t)((B - b_last) * (int64_t)cpi), CT = (uint32_t)kWarps * GS;
-  const uint32_t nT = (GB + CT - 1) / CT;
-  if (tid < kRing) ring_tag[tid] = -1;
-  if (tid < kWarps) ring_read[tid] = 0;
-  if (tid == 0) ring_claim = 0;
-  __syncthreads();
-  int tix = -1;           // CTA ticket index this warp is on
-  uint32_t tcur = 0, tm = GS;  // its global ticket, chunks taken from it
-  auto cta_ticket = [&](int i) -> uint32_t {  // lane 0: the CTA's i-th ticket
-    volatile int* tag = ring_tag;
-    volatile uint32_t* rt = ring_t;
-    for (;;) {
-      if (tag[i % kRing] == i) break;
-      if (*(volatile int*)&ring_claim == i && atomicCAS(&ring_claim, i, i + 1) == i) {
-        for (bool ok = false; !ok;) {  // every warp has read ticket i - kRing (slot free)
-          ok = true;
-          for (int u = 0; u < kWarps; ++u) ok = ok && ((volatile int*)ring_read)[u] > i - kRing;
-        }
-        rt[i % kRing] = atomicAdd(ticket, 1u);
-        __threadfence_block();
-        tag[i % kRing] = i;
-        break;
-      }
-      __nanosleep(20);
-    }
-    const uint32_t t = rt[i % kRing];
-    __threadfence_block();
-    ((volatile int*)ring_read)[w] = i + 1;
-    return t;
-  };
-  const uint64_t pol = policy_evict_first();
-  uint2* tab = s.tab[w];
-  // loader state (lane 0): image and chunk range of the current group, prefetched next ticket
-  uint32_t lb = 0, lc = 0, le = 0, nxt = 0, rd_img = kEndImg;
-  if (lane == 0 && b_last == 0) nxt = atomicAdd(ticket, 1u);
-  auto next_chunk = [&](uint32_t& b, uint32_t& c) -> bool {
-    if (sA < nA) {  // static part
-      const uint32_t g = a0 + (uint32_t)w + sA * kWarps;
-      ++sA;
-      b = g / cpi;
-      c = g - b * cpi;
-      if (ready && b != rd_img) {
-        while (ld_acquire(ready + b) == 0u) __nanosleep(100);
-        rd_img = b;
-      }
-      return true;
-    }
-    if (b_last > 0) {  // part B: CTA tickets
-      for (;;) {
-        if (tm >= GS) {
-          tcur = cta_ticket(++tix);
-          tm = 0;
-        }
-        if (tcur >= nT) {
-          ((volatile int*)ring_read)[w] = 1 << 30;  // never blocks a refill again
-          return false;
-        }
-        const uint32_t g = tcur * CT + (uint32_t)w + tm * kWarps;
-        ++tm;
-        if (g >= GB) {
-          tm = GS;
-          continue;
-        }
-        b = (uint32_t)b_last + g / cpi;
-        c = g % cpi;
-        break;
-      }
-      if (ready && b != rd_img) {
-        while (ld_acquire(ready + b) == 0u) __nanosleep(100);
-        rd_img = b;
-      }
-      return true;
-    }
-    if (lc >= le) {
-      if (nxt >= ngroups) return false;
-      const uint32_t q = (uint32_t)b_last + nxt / gpi, g = nxt % gpi;
-      if (queue) {
-        uint32_t v;
-        while ((v = ld_acquire(queue + q)) == 0u) __nanosleep(100);
-        lb = v - 1u;
-      } else {
-        lb = q;
-        if (ready && q != rd_img) {  // natural order gated by the image's LUT-ready flag
-          while (ld_acquire(ready + q) == 0u) __nanosleep(100);
-          rd_img = q;
-        }
-      }
-      lc = g * GS;
-      le = min(lc + GS, cpi);
-      nxt = atomicAdd(ticket, 1u);
-    }
-    b = lb;
-    c = lc++;
-    return true;
-  };
-  uint32_t ld_img = kEndImg, pend_img = kEndImg;
-  uint2 pend = make_uint2(0u, 0u);
-  auto issue = [&](uint32_t i) {  // all lanes; lane 0 fills stage i % kStages
-    const int st = (int)(i % kStages);
-    uint32_t b = kEndImg, c = 0;
-    if (lane == 0 && !next_chunk(b, c)) b = kEndImg;
-    b = __shfl_sync(0xffffffffu, b, 0);
-    c = __shfl_sync(0xffffffffu, c, 0);
-    __syncwarp();  // lane 0's queue acquire before the other lanes read this image's LUT
-    if (lane == 0) meta[w][st] = make_uint2(b, c);
-    if (b == kEndImg) {
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s.bar[w][st])) : "memory");
-      return;
-    }
-    if (b != ld_img) {
-      ld_img = b;
-      if (pend_img == kEndImg) {
-        pend = __ldcg(reinterpret_cast<const uint2*>(lut + (uint64_t)b * kLevels) + lane);
-        pend_img = b;
-      }
-    }
-    if (lane == 0) {
-      const uint32_t px0 = c * kChunkPx, npx = min((uint32_t)kChunkPx, (uint32_t)(HW - px0));
-      const uint64_t off = ((uint64_t)b * (uint64_t)HW + px0) * 3u;
-      mbar_expect_tx(&s.bar[w][st], npx * 3u);
-      bulk_load(s.stage[w][st], in + off, npx * 3u, &s.bar[w][st], pol);
-    }
-  };
-  for (uint32_t i = 0; i < (uint32_t)kAhead; ++i) issue(i);
-  uint32_t cur_img = kEndImg;
-  int st = 0;
-  uint32_t ph = 0;
-  for (uint32_t i = 0;; ++i) {
-    if (lane == 0 && i >= 2) bulk_wait_read<1>();
-    __syncwarp();
-    issue(i + kAhead);
-    mbar_wait(&s.bar[w][st], ph);
-    const uint2 m = meta[w][st];
-    if (m.x == kEndImg) break;  // warp-uniform
-    const uint32_t b = m.x, px0 = m.y * kChunkPx;
-    const uint32_t bytes = min((uint32_t)kChunkPx, (uint32_t)(HW - px0)) * 3u;
-    const uint64_t off = ((uint64_t)b * (uint64_t)HW + px0) * 3u;
-    HR_CHECK(b < B && bytes > 0 && bytes <= (uint32_t)kChunkBytes);
-    if (b != cur_img) {
-      __syncwarp();
-      if (b == pend_img) {
-        build_tab_regs(tab, pend, lane);
-        pend_img = kEndImg;
-      } else {
-        build_tab(tab, lut + (uint64_t)b * kLevels, lane);  // queue order implies the LUT is done
-      }
-      __syncwarp();
-      cur_img = b;
-    }
-    uint8_t* p = s.stage[w][st];
-    apply_chunk_smem(p, bytes, tab, lane);
-    fence_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      bulk_store(out + off, p, bytes, pol);
-      bulk_commit();
-    }
-    if (++st == kStages) {
-      st = 0;
-      ph ^= 1u;
-    }
-  }
-  if (lane == 0) bulk_wait<0>();
-  TRACE_END(5u, 0u, 0ull);
-}
-
 // ---------------------------------------------------------------- scalar fallback
 __device__ __forceinline__ void apply_scalar(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int64_t q,
                                              const uint32_t* ab) {
@@ -400,63 +169,31 @@ k_apply_scalar(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, 
 
 }  // namespace
 
-void trace_bind_apply(void* buf, uint32_t* n, uint32_t cap) {
-#ifdef HR_STEP_TRACE
-  trace_bind_tu(buf, n, cap);
-#else
-  (void)buf, (void)n, (void)cap;
-#endif
-}
+cudaError_t trace_bind_apply(void* buf, uint32_t* n, uint32_t cap) { return trace_bind_tu(buf, n, cap); }
 
-bool apply_dyn_supported(const uint8_t* in, const uint8_t* out, int64_t B, int32_t H, int32_t W) {
-  const int64_t HW = (int64_t)H * W;
-  return reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 && HW % 16 == 0 &&
-         B * ((HW + kChunkPx - 1) / kChunkPx) < (1LL << 31);
-}
-
-cudaError_t launch_apply_dyn(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
-                             int grid_ctas, const uint32_t* queue, uint32_t* ticket, int GS, cudaStream_t st,
-                             const uint32_t* ready, int64_t b_last) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_apply_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(ApplySmem) + sizeof(DynSmem)));
-    // the whole carve-out: without it the driver may configure less shared memory than two
-    // CTAs need, halving the resident warps (measured 1.5x slower)
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_apply_dyn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               (int)cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const int64_t HW = (int64_t)H * W;
-  return launch_pdl(k_apply_dyn, dim3((unsigned)(grid_ctas < 1 ? 1 : grid_ctas)), dim3(kApplyThreads),
-                    sizeof(ApplySmem) + sizeof(DynSmem), st, in, lut, B, HW, out, queue, ticket, (uint32_t)(GS < 1 ? 1 : GS), ready, b_last);
+cudaError_t init_attrs_apply() {
+  cudaError_t e = cudaFuncSetAttribute(k_apply_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ApplySmem));
+  // the whole carve-out: without it the driver may configure less shared memory than two CTAs
+  // need, halving the resident warps (measured 1.5x slower)
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_apply_tma, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
+  return e;
 }
 
 cudaError_t launch_apply(const uint8_t* in, const uint8_t* lut, int64_t B, int32_t H, int32_t W, uint8_t* out,
                          int grid_ctas, cudaStream_t st, const uint32_t* ready, int64_t b_last, uint32_t* ticket,
-                         int GS, int tail_pct) {
+                         int GS) {
   const int64_t HW = (int64_t)H * W;
   const bool tma = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
                    (HW % 16 == 0) && B * ((HW + kChunkPx - 1) / kChunkPx) < (1LL << 31);
   if (tma) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k_apply_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)sizeof(ApplySmem));
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_apply_tma, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 (int)cudaSharedmemCarveoutMaxShared);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
     const int64_t chunks = B * ((HW + kChunkPx - 1) / kChunkPx);
     int64_t grid = grid_ctas;
     if (grid > (chunks + kWarps - 1) / kWarps) grid = (chunks + kWarps - 1) / kWarps;
     if (grid < 1) grid = 1;
     return launch_pdl(k_apply_tma, dim3((unsigned)grid), dim3(kApplyThreads), sizeof(ApplySmem), st, in, lut, B, HW,
-                      out, ready, b_last, ticket, (uint32_t)(GS < 1 ? 1 : GS), (uint32_t)(tail_pct < 0 ? 0 : tail_pct));
+                      out, ready, b_last, ticket, (uint32_t)(GS < 1 ? 1 : GS));
   } else {
     int64_t grid = 4LL * grid_ctas;
     const int64_t P = B * HW;

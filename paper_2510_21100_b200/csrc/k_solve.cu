@@ -25,46 +25,17 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_solve(SolveArgs args) {
   } else {
     pdl_trigger();
   }
-  // one image per CTA, or (nimg > 0) images blockIdx.x, blockIdx.x + gridDim.x, ... in turn
-  const int64_t n = args.nimg > 0 ? args.nimg : (int64_t)gridDim.x;
-  __shared__ int64_t b_s;
-  for (int64_t bi = blockIdx.x; bi < n; bi += gridDim.x) {
-    int64_t b = bi;
-    if (args.cq) {  // the next image in histogram-completion order (complete by construction)
-      if (threadIdx.x == 0) {
-        const uint32_t pos = atomicAdd(args.cq_head, 1u);
-        uint32_t v;
-        long long spins = 0;
-        while ((v = ld_acquire(args.cq + pos)) == 0u) {
-          __nanosleep(128);
-          if (++spins > (1LL << 25)) asm volatile("trap;");  // ~10 s: a logic error, not a wait
-        }
-        b_s = (int64_t)v - 1;
-      }
-      __syncthreads();
-      b = b_s;
-    } else if (args.hist_done) {  // overlap the histogram pass: wait for this image's rows only
-      if (threadIdx.x == 0) {
-        const uint32_t need = (uint32_t)args.hist_H;
-        long long spins = 0;
-        while (ld_acquire(args.hist_done + b) < need) {
-          __nanosleep(256);
-          if (++spins > (1LL << 25)) asm volatile("trap;");  // ~10 s: a logic error, not a wait
-        }
-      }
-      __syncthreads();
-    }
-    TRACE_MID(tr_mid);
-    solve_image<NT>(args, b, smraw, wscr);
-    __syncthreads();  // every exit of solve_image arrives here: LUT written, shared state free
-    if (args.ready || args.queue) {
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        if (args.ready) st_release(args.ready + b, 1u);
-        if (args.queue) st_release(args.queue + atomicAdd(args.queue_tail, 1u), (uint32_t)b + 1u);
-      }
-    }
+  const int64_t b = blockIdx.x;
+  if (args.hist_done) {  // wait for this image's histogram rows only (all H rows flushed)
+    if (threadIdx.x == 0) wait_flag_geq(args.hist_done + b, (uint32_t)args.hist_H, 256);
+    __syncthreads();
+  }
+  TRACE_MID(tr_mid);
+  solve_image<NT>(args, b, smraw, wscr);
+  if (args.ready) {  // every exit of solve_image arrives here: the LUT is written
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(args.ready + b, 1u);
   }
   TRACE_END(3u, (uint32_t)((uintptr_t)args.hist_s >> 8), tr_mid);  // aux: which launch (group)
 }
@@ -103,42 +74,34 @@ __global__ void __launch_bounds__(kLevels) k_match(const uint32_t* hist_s, const
 
 }  // namespace
 
-void trace_bind_solve(void* buf, uint32_t* n, uint32_t cap) {
-#ifdef HR_STEP_TRACE
-  trace_bind_tu(buf, n, cap);
-#else
-  (void)buf, (void)n, (void)cap;
-#endif
-}
+cudaError_t trace_bind_solve(void* buf, uint32_t* n, uint32_t cap) { return trace_bind_tu(buf, n, cap); }
 
 size_t solve_smem_bytes(int arena_bytes) { return sizeof(Sm) + (size_t)(arena_bytes > 0 ? arena_bytes : kArenaSmem); }
 size_t solve_cells_ws_bytes(int64_t B) { return (size_t)B * (size_t)kArenaGlobal; }
+
+constexpr int kBigArena = 190 * 1024;  // sizeof(Sm) + 190 KB <= 227 KB per block
+
+cudaError_t init_attrs_solve() {
+  cudaError_t e = cudaSuccess;
+  for (auto k : {k_solve<256>, k_solve<512>}) {
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem_bytes(kBigArena));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+  }
+  return e;
+}
 
 // cpsm == 1: one solver CTA per SM (the CTA scheduler would otherwise pack two latency-bound
 // solves onto one SM while others idle).  The shared memory that placement reserves anyway is
 // given to the run arena (kBigArena), so images with large supports (C4: E = 8480 cells) keep
 // their run structure in shared memory instead of the global arena.
-cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t st, int max_ctas, bool wide) {
-  constexpr int kBigArena = 190 * 1024;  // sizeof(Sm) + 190 KB <= 227 KB per block
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaSuccess;
-    for (auto k : {k_solve<256>, k_solve<512>}) {
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem_bytes(kBigArena));
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    }
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t st, bool wide) {
   SolveArgs a = a0;
   if (cpsm == 1 && a.arena_bytes == 0) a.arena_bytes = kBigArena;
-  const int64_t grid = max_ctas > 0 ? std::min<int64_t>(B, max_ctas) : B;
-  a.nimg = grid < B ? B : 0;  // fewer CTAs than images: each CTA solves several in turn
   if (cpsm == 1 && wide)
-    return launch_pdl(k_solve<512>, dim3((unsigned)grid), dim3(512), solve_smem_bytes(a.arena_bytes), st, a);
-  return launch_pdl(k_solve<256>, dim3((unsigned)grid), dim3(256), solve_smem_bytes(a.arena_bytes), st, a);
+    return launch_pdl(k_solve<512>, dim3((unsigned)B), dim3(512), solve_smem_bytes(a.arena_bytes), st, a);
+  return launch_pdl(k_solve<256>, dim3((unsigned)B), dim3(256), solve_smem_bytes(a.arena_bytes), st, a);
 }
 
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st) {

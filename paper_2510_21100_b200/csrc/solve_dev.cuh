@@ -1,6 +1,5 @@
 // solve_dev.cuh -- device body of kernel (b): one image of the histogram-domain Retinex
-// solver (Algorithm 1, fp64) + Eq. 20 + the CDF/LUT tail (c).  Shared by k_solve (k_solve.cu)
-// and the persistent fused kernel (k_fused.cu).
+// solver (Algorithm 1, fp64) + Eq. 20 + the CDF/LUT tail (c), launched by k_solve (k_solve.cu).
 //
 //
 // One CTA (256 threads) per image, 2 CTAs per SM.  PAPER.md references:
@@ -702,8 +701,8 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
 
 // One image of Algorithm 1 + Eq. 20 + the CDF/LUT tail, by all T threads of the CTA.
 // smraw: solve_smem_bytes() of shared memory; wscr: NW ints of shared scratch.  Every exit is
-// CTA-uniform.  Histograms are read through L2 (__ldcg): in the fused kernel they were
-// accumulated by other CTAs' atomics during this launch.
+// CTA-uniform.  Histograms are read through L2 (__ldcg): in the grouped step they were
+// accumulated by other grids' atomics while this grid was already running.
 template <int T>
 __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t b, unsigned char* smraw, int* wscr) {
 #ifdef HR_SOLVE_PROFILE
@@ -717,7 +716,6 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   uint32_t* mask = reinterpret_cast<uint32_t*>(arenaS + AB - kMaskBytes);
   const int tid = threadIdx.x;
   const hr_params& P = args.p;
-  if (args.only_deferred && args.only_deferred[b] == 0) return;  // solved by k_solve_warp
 
   // ---- histograms (Alg. 1 init) ----
   constexpr int NW = T / 32;

@@ -134,31 +134,24 @@ def test_histogram_ragged_shapes(shape):
         assert np.array_equal(hgr.cpu().numpy()[b, :511].astype(np.uint64), oracle.count_histogram(g, 511))
 
 
-# Shapes that take the TMA-staged histogram kernel (W % 16 == 0 with W >= 256: 48-B strips;
-# W % 16 == 8 with W >= 128 and the batch's byte count a multiple of 16: 24-B strips with
-# rows alternating 0 / 8 bytes of misalignment, odd H misaligns image bases) and, for
-# comparison, the direct-load kernel (hist_tma = 0).  Strong edges (uniform noise: gradients
-# up to 510) exercise the checked gradient path; tiny batches give 1-row bands and groups
-# without rows; a tall image gives long walks (many pipeline stages per band).
+# Strip-walk shapes of the histogram kernel: W % 16 == 0 (48-B strips), W % 16 == 8 (rows
+# alternating 0 / 8 bytes of misalignment, half strips; odd H misaligns image bases).  Strong
+# edges (uniform noise: gradients up to 510) exercise the checked gradient path; tiny batches
+# give 1-row bands and groups without rows; a tall image gives long walks.
 TMA_SHAPES = [(2, 33, 256, "img"), (2, 37, 264, "img"), (3, 8, 1920, "noise"), (2, 37, 264, "noise"),
               (1, 200, 600, "img"), (2, 41, 1000, "noise"), (1, 2400, 1920, "img"), (4, 1, 16384, "noise"), (1, 600, 16384, "noise"),
               (1, 3000, 136, "img")]
 
 
 @pytest.mark.parametrize("shape", TMA_SHAPES)
-@pytest.mark.parametrize("tma", [1, 0])
-def test_histogram_tma_kernel(shape, tma):
+def test_histogram_walk_shapes(shape):
     B, H, W, kind = shape
     if kind == "noise":
         x = np.random.default_rng(H * W + B).integers(0, 256, size=(B, H, W, 3), dtype=np.uint8)
     else:
         x = np.stack([synth.make_image(H, W, seed=300 + b, peak=0.05 + 0.2 * b) for b in range(B)])
-    hr().set_policy("hist_tma", tma)
-    try:
-        hs, hg, hgr = hr().hr_histogram(to_dev(x))
-        hs, hgr = hs.cpu().numpy(), hgr.cpu().numpy()
-    finally:
-        hr().set_policy("hist_tma", 0)
+    hs, hg, hgr = hr().hr_histogram(to_dev(x))
+    hs, hgr = hs.cpu().numpy(), hgr.cpu().numpy()
     for b in range(B):
         S = oracle.value_channel(x[b])
         assert np.array_equal(hs[b].astype(np.uint64), oracle.count_histogram(S, 256)), f"hist_s {b}"

@@ -1,7 +1,7 @@
-"""Per-CTA end times of the histogram kernel vs its segment count (measurement build
-tools/libhistretinex_steptrace.so; not product code).
+"""Per-CTA end times of the histogram kernel vs its segment count (step trace via
+hr_trace_bind; not product code).
 
-    HR_LIB=tools/libhistretinex_steptrace.so python tools/hist_balance.py C5
+    python tools/hist_balance.py C5
 """
 import sys
 
@@ -17,14 +17,13 @@ REC = np.dtype([("kind", "<u4"), ("cta", "<u4"), ("sm", "<u4"), ("aux", "<u4"), 
                 ("t1", "<u8"), ("pad", "<u8")])
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
 lib = _lib.load()
-lib.hr_debug_trace_bind.argtypes = [__import__("ctypes").c_void_p] * 2 + [__import__("ctypes").c_uint32]
 cap = 1 << 16
 buf = torch.zeros(cap * REC.itemsize, dtype=torch.uint8, device="cuda")
 cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
 x = torch.from_numpy(synth.make_config(cfg)).cuda()
 B, H, W, _ = x.shape
 hs, hg, hgr = hr.hr_histogram(x)
-lib.hr_debug_trace_bind(buf.data_ptr(), cnt.data_ptr(), cap)
+hr.trace_bind(buf, cnt, cap)
 ends = []
 for rep in range(5):
     cnt.zero_()

@@ -89,7 +89,7 @@ def summarise_launches(tag, spec):
         if len(r) <= vi:
             continue
         k = r[ki]
-        for short in ("k_fused", "k_hist", "k_solve_warp", "k_solve", "k_apply", "k_remap", "k_match", "k_idx1_table"):
+        for short in ("k_hist", "k_solve", "k_apply", "k_remap", "k_match", "k_idx1_table"):
             if short in k:
                 k = short
                 break

@@ -1,10 +1,9 @@
-"""Timeline of one hr_enhance step (measurement build tools/libhistretinex_steptrace.so,
--DHR_STEP_TRACE): per kernel the CTA start/end spread, per solver CTA its wait for the image's
-histogram and its solve, and when the apply CTAs start.  Not product code.
+"""Timeline of one hr_enhance step (step trace via hr_trace_bind): per kernel the CTA
+start/end spread, per solver CTA its wait for the image's histogram and its solve, and when the
+apply CTAs start.  Not product code.
 
-    HR_LIB=tools/libhistretinex_steptrace.so python tools/step_trace.py C3 [ENV=VAL ...]
+    python tools/step_trace.py C3 [ENV=VAL ...]
 """
-import ctypes
 import os
 import sys
 
@@ -18,7 +17,7 @@ from paper_2510_21100_b200 import _lib  # noqa: E402
 
 REC = np.dtype([("kind", "<u4"), ("cta", "<u4"), ("sm", "<u4"), ("aux", "<u4"), ("t0", "<u8"), ("mid", "<u8"),
                 ("t1", "<u8"), ("pad", "<u8")])
-NAMES = {1: "k_hist", 2: "k_hist_tma", 3: "k_solve", 4: "k_apply", 5: "k_apply_dyn"}
+NAMES = {1: "k_hist", 3: "k_solve", 4: "k_apply"}
 
 
 def pct(a, qs=(0, 10, 50, 90, 100)):
@@ -28,7 +27,6 @@ def pct(a, qs=(0, 10, 50, 90, 100)):
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
     lib = _lib.load()
-    lib.hr_debug_trace_bind.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32]
     cap = 1 << 16
     buf = torch.zeros(cap * REC.itemsize, dtype=torch.uint8, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -38,7 +36,7 @@ def main():
     for _ in range(5):
         hr.hr_enhance(x, out=out, workspace=ws)
     torch.cuda.synchronize()
-    assert lib.hr_debug_trace_bind(buf.data_ptr(), cnt.data_ptr(), cap) == 0
+    hr.trace_bind(buf, cnt, cap)
     for _ in range(3):  # keep the last of three back-to-back steps (as in the bench loop)
         cnt.zero_()
         torch.cuda.synchronize()
