@@ -18,7 +18,12 @@ import tempfile
 def sass_lines(lib, kname):
     """{offset: (file, line)} for the first function whose name contains kname."""
     tmp = tempfile.mkdtemp()
-    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
+    if lib.endswith(".cubin"):
+        import shutil
+
+        shutil.copy(lib, tmp)
+    else:
+        subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
     out = {}
     for f in sorted(os.listdir(tmp)):
         if not f.endswith(".cubin"):
