@@ -150,8 +150,8 @@ hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_de
    image groups, policy "groups": the second group's histograms run beside the first group's
    solves, the apply beside the second group's solves).  Every policy gives bit-identical
    outputs.  The first call with a new gamma builds its index_1 table (Eqs. 17-19) and waits for
-   it (host-blocking, once per gamma per context).  Optional debug outputs (device, nullable):
-   hist_s [B][256], lut [B][256], iters [B] (hr_enhance_debug).  rgb_out must not alias rgb_in.
+   it (host-blocking, once per gamma per context).  Intermediate results: hr_enhance_debug.
+   rgb_out must not alias rgb_in.
    Workspace: hr_workspace_bytes(B,H,W), device. */
 hr_status hr_enhance(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H, int32_t W,
                      const hr_params* params, uint8_t* rgb_out_dev, void* ws_dev, void* stream);
@@ -170,10 +170,22 @@ hr_status hr_enhance_host(hr_ctx* ctx, const uint8_t* rgb_in_host, int64_t B, in
                           const hr_params* params, uint8_t* rgb_out_host, uint8_t* in_dev, uint8_t* out_dev,
                           void* ws_dev, int32_t chunks, void* stream);
 
-hr_status hr_enhance_debug(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H,
-                           int32_t W, const hr_params* params, uint8_t* rgb_out_dev, void* ws_dev,
-                           uint32_t* hist_s_dev, uint8_t* lut_dev, int32_t* iters_dev,
-                           void* stream);
+/* hr_enhance with intermediate results (parity tests): every non-NULL field receives, for the
+   same schedule and launch configuration as hr_enhance, the image's hist_s / hist_g (the
+   gradient levels of R14) [B][256] uint32, lut [B][256], iters [B], and the solver's final hL,
+   hR and Eq. 20 target [B][256] double (device pointers, caller-owned).  dbg may be NULL. */
+typedef struct hr_debug_out {
+  uint32_t* hist_s;
+  uint32_t* hist_g;
+  uint8_t* lut;
+  int32_t* iters;
+  double* hL;
+  double* hR;
+  double* target;
+} hr_debug_out;
+hr_status hr_enhance_debug(hr_ctx* ctx, const uint8_t* rgb_in_dev, int64_t B, int32_t H, int32_t W,
+                           const hr_params* params, uint8_t* rgb_out_dev, void* ws_dev,
+                           const hr_debug_out* dbg, void* stream);
 
 /* ---- Second workload: the HE baseline and the quality metrics ---- */
 

@@ -353,19 +353,27 @@ def kernel_launches(device=None) -> int:
     return int(_lib.load().hr_kernel_launches(_context(dev)))
 
 
-def hr_enhance_debug(rgb: torch.Tensor, params: Params | None = None):
-    """hr_enhance also returning the intermediate hist_s, lut and iteration counts."""
+def hr_enhance_debug(rgb: torch.Tensor, params: Params | None = None, full: bool = False):
+    """hr_enhance also returning intermediate results of the same schedule: (out, hist_s, lut,
+    iters), or with full=True a dict with out, hist_s, hist_g, lut, iters, hL, hR, target."""
     p = params or Params()
     x = _images(rgb)
     B, H, W, _ = x.shape
     dev = x.device
     out = torch.empty_like(x)
-    hs = torch.empty((B, 256), dtype=torch.int32, device=dev)
-    lut = torch.empty((B, 256), dtype=torch.uint8, device=dev)
-    it = torch.empty((B,), dtype=torch.int32, device=dev)
+    r = {"out": out,
+         "hist_s": torch.empty((B, 256), dtype=torch.int32, device=dev),
+         "lut": torch.empty((B, 256), dtype=torch.uint8, device=dev),
+         "iters": torch.empty((B,), dtype=torch.int32, device=dev)}
+    if full:
+        r["hist_g"] = torch.empty((B, 256), dtype=torch.int32, device=dev)
+        for k in ("hL", "hR", "target"):
+            r[k] = torch.empty((B, 256), dtype=torch.float64, device=dev)
+    dbg = _lib.HrDebugOut(*[r[k].data_ptr() if k in r else None
+                            for k in ("hist_s", "hist_g", "lut", "iters", "hL", "hR", "target")])
     ws = _workspace(B, H, W, dev)
     pc = p.c()
     ctx = _context(dev)
     _check(_lib.load().hr_enhance_debug(ctx, _ptr(x), B, H, W, ctypes.byref(pc), _ptr(out), _ptr(ws),
-                                        _ptr(hs), _ptr(lut), _ptr(it), _stream(dev)), ctx)
-    return out, hs, lut, it
+                                        ctypes.byref(dbg), _stream(dev)), ctx)
+    return r if full else (out, r["hist_s"], r["lut"], r["iters"])

@@ -24,6 +24,12 @@ EXPORTS = (
 )
 
 
+class HrDebugOut(ctypes.Structure):
+    """Mirror of ``hr_debug_out`` (include/histretinex.h): nullable device pointers."""
+
+    _fields_ = [(n, ctypes.c_void_p) for n in ("hist_s", "hist_g", "lut", "iters", "hL", "hR", "target")]
+
+
 class HrParams(ctypes.Structure):
     """Mirror of ``hr_params`` (include/histretinex.h)."""
 
@@ -76,7 +82,7 @@ def load() -> ctypes.CDLL:
         "hr_match": ([vp, vp, vp, i64, vp, vp, vp], i32),
         "hr_apply": ([vp, vp, vp, i64, i32, i32, vp, vp], i32),
         "hr_enhance": ([vp, vp, i64, i32, i32, P, vp, vp, vp], i32),
-        "hr_enhance_debug": ([vp, vp, i64, i32, i32, P, vp, vp, vp, vp, vp, vp], i32),
+        "hr_enhance_debug": ([vp, vp, i64, i32, i32, P, vp, vp, ctypes.POINTER(HrDebugOut), vp], i32),
         "hr_enhance_host": ([vp, vp, i64, i32, i32, P, vp, vp, vp, vp, i32, vp], i32),
         "hr_profile_enable": ([vp, i32], i32),
         "hr_profile_collect": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)], i32),

@@ -456,8 +456,7 @@ hr_status hr_apply(hr_ctx* c, const uint8_t* in, const uint8_t* lut, int64_t B, 
 }
 
 hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, const hr_params* p,
-                           uint8_t* out, void* ws, uint32_t* hist_s_dbg, uint8_t* lut_dbg, int32_t* iters_dbg,
-                           void* stream) {
+                           uint8_t* out, void* ws, const hr_debug_out* dbg, void* stream) {
   if (!c) return HR_EINVAL;
   hr_status s = check_shape(c, B, H, W);
   if (s) return s;
@@ -480,12 +479,14 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
   }
   auto mark = [&](int k) -> cudaError_t { return ev ? cudaEventRecord(ev[k], st) : cudaSuccess; };
   const WsLayout L = ws_layout(B);
-  uint32_t* hs = hist_s_dbg ? hist_s_dbg : reinterpret_cast<uint32_t*>((char*)ws + L.hist_s);
+  const hr_debug_out none{};
+  const hr_debug_out& D = dbg ? *dbg : none;
+  uint32_t* hs = D.hist_s ? D.hist_s : reinterpret_cast<uint32_t*>((char*)ws + L.hist_s);
   uint32_t* graw = reinterpret_cast<uint32_t*>((char*)ws + L.graw);
   uint32_t* ctl = reinterpret_cast<uint32_t*>((char*)ws + L.ctl);
   uint32_t* done = ctl + hr::kCtlHeader;  // rows flushed per image (k_hist -> k_solve)
   uint32_t* ready = done + B;             // LUT written per image (k_solve -> k_apply)
-  uint8_t* lut = lut_dbg ? lut_dbg : reinterpret_cast<uint8_t*>((char*)ws + L.lut);
+  uint8_t* lut = D.lut ? D.lut : reinterpret_cast<uint8_t*>((char*)ws + L.lut);
   unsigned char* cells = reinterpret_cast<unsigned char*>((char*)ws + L.cells);
   const uint8_t* tab = nullptr;
   int slot = 0;
@@ -507,7 +508,11 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     a.graw = graw + b0 * kGradSlots;
     a.grad_norm = p->grad_norm;
     a.p = *p;
-    a.iters = iters_dbg ? iters_dbg + b0 : nullptr;
+    a.iters = D.iters ? D.iters + b0 : nullptr;
+    a.hist_g_out = D.hist_g ? D.hist_g + b0 * kLevels : nullptr;
+    a.hL = D.hL ? D.hL + b0 * kLevels : nullptr;
+    a.hR = D.hR ? D.hR + b0 * kLevels : nullptr;
+    a.target = D.target ? D.target + b0 * kLevels : nullptr;
     a.lut = lut + b0 * kLevels;  // CDF + LUT tail fused into the solver CTA (no target round trip)
     a.cells_ws = cells + (size_t)b0 * hr::solve_cells_ws_bytes(1);
     // 512-thread solver CTAs for large images (their supports, and so the cell loops, tend to be
@@ -576,7 +581,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
 
 hr_status hr_enhance(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, const hr_params* p,
                      uint8_t* out, void* ws, void* stream) {
-  return hr_enhance_debug(c, in, B, H, W, p, out, ws, nullptr, nullptr, nullptr, stream);
+  return hr_enhance_debug(c, in, B, H, W, p, out, ws, nullptr, stream);
 }
 
 hr_status hr_he(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, uint8_t* out, uint8_t* lut_dbg,
@@ -651,8 +656,7 @@ hr_status hr_enhance_host(hr_ctx* c, const uint8_t* in_h, int64_t B, int32_t H, 
     const int64_t b0 = B * k / K, nb = B * (k + 1) / K - b0;
     e = cudaStreamWaitEvent(st, E[2 + k], 0);
     if (e != cudaSuccess) break;
-    const hr_status r = hr_enhance_debug(c, in_d + b0 * img, nb, H, W, p, out_d + b0 * img, ws, nullptr, nullptr,
-                                         nullptr, stream);
+    const hr_status r = hr_enhance_debug(c, in_d + b0 * img, nb, H, W, p, out_d + b0 * img, ws, nullptr, stream);
     if (r != HR_OK) return r;
     e = cudaEventRecord(E[2 + K + k], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c->sOut, E[2 + K + k], 0);

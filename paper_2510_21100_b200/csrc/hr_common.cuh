@@ -170,6 +170,7 @@ cudaError_t launch_remap(const uint32_t* hist_graw, int64_t B, int32_t grad_norm
 struct SolveArgs {
   const uint32_t* hist_s;   // [B][256]
   const uint32_t* hist_g;   // [B][256] remapped gradient histogram, or NULL -> use graw
+  uint32_t* hist_g_out;     // [B][256] nullable: the remapped gradient histogram (debug output)
   const uint32_t* graw;     // [B][512] raw gradient histogram (used when hist_g == NULL)
   int32_t grad_norm;        // remap mode when reading graw
   hr_params p;

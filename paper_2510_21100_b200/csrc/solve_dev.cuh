@@ -729,6 +729,7 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   if (binT) {
     s.bk[tid] = (double)tid / 255.0;
     s.hSd[tid] = (double)s.hSi[tid];
+    if (args.hist_g_out) args.hist_g_out[b * kLevels + tid] = s.hGi[tid];
   }
   __syncthreads();
   PROF_MARK();
