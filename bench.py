@@ -372,7 +372,21 @@ def run_ours(args, world, rank, local):
     out = torch.empty_like(x)
     out_pin = torch.empty_like(x_pin, pin_memory=True)
     ws = torch.empty(hr.workspace_bytes(B, H, W), dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    # a stream of our own (not the legacy default stream): single-image steps are then
+    # replayed from the library's cached CUDA graph (policy graph_b1)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(stream):
+        run_ours_on_stream(args, world, rank, local, dev, dist, hr, synth, cfg, B, H, W, params, x_pin, x, out, out_pin,
+                           ws, stream)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_ours_on_stream(args, world, rank, local, dev, dist, hr, synth, cfg, B, H, W, params, x_pin, x, out, out_pin,
+                       ws, stream):
+    import torch
 
     def step():
         hr.hr_enhance(x, params, out=out, workspace=ws)
@@ -492,6 +506,8 @@ def run_ours(args, world, rank, local):
                      "last group's solves)")
     else:
         path_name = "separate kernels (hist | solve + LUT | apply)"
+        if B == 1 and hr.get_policy("graph_b1", local):
+            path_name += ", replayed as one CUDA graph per step"
     value = aggregate_mps(world, B, H, W, ms)
     peak, peak_src = peaks()
     step_bytes = BYTES_PER_PX * B * H * W
@@ -545,9 +561,6 @@ def run_ours(args, world, rank, local):
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
 
 
 def main():

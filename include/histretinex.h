@@ -148,8 +148,9 @@ hr_status hr_apply(hr_ctx* ctx, const uint8_t* rgb_in_dev, const uint8_t* lut_de
    apply kernels in order, chained by programmatic dependent launch, the apply acquiring each
    image's LUT-ready flag (so it overlaps the solver's tail).  B >= 2: the grouped step (two
    image groups, policy "groups": the second group's histograms run beside the first group's
-   solves, the apply beside the second group's solves).  Every policy gives bit-identical
-   outputs.  The first call with a new gamma builds its index_1 table (Eqs. 17-19) and waits for
+   solves, the apply beside the second group's solves).  One image on a non-default stream
+   (policy graph_b1): the step's launches are captured once into a CUDA graph, cached per
+   call arguments, and replayed.  Every policy gives bit-identical outputs.  The first call with a new gamma builds its index_1 table (Eqs. 17-19) and waits for
    it (host-blocking, once per gamma per context).  Intermediate results: hr_enhance_debug.
    rgb_out must not alias rgb_in.
    Workspace: hr_workspace_bytes(B,H,W), device. */
@@ -257,6 +258,11 @@ hr_status hr_trace_bind(hr_ctx* ctx, void* records_dev, uint32_t* count_dev, uin
                     group's few solves beside the first group's apply, C5 0.167 vs 0.177)
      "apply_gs"     grouped step's apply: 1024-pixel chunks per warp in one CTA  default 8
                     ticket of the last group (>= 1)
+     "graph_b1"     hr_enhance with B == 1 on a non-default stream: the step is     default 1
+                    captured once into a CUDA graph (cached per call arguments,
+                    8 entries, LRU) and replayed (C1/C2/C4 1.5-2 us faster; batches
+                    launch directly: they lose the PDL overlap of consecutive steps
+                    in a graph)
    The environment variables HR_<KEY upper-cased> set the initial values at hr_create.
    Returns HR_EINVAL for an unknown key or an out-of-range value (nothing changes). */
 hr_status hr_set_policy(hr_ctx* ctx, const char* key, int64_t value);

@@ -174,6 +174,21 @@ __device__ __forceinline__ void grad_row(uint32_t sb, uint32_t* ghi, uint32_t Lg
   }
 }
 
+// L2 prefetch of one image row (bulk async prefetch, no registers held): [row, row + bytes)
+// widened to 16-B alignment and clamped to the image end (aligned down), so it never leaves
+// the caller's buffer.  Issued a few rows ahead of the walk by the first thread of each row
+// group: the walk's own loads (one row ahead, registers) then hit L2 instead of DRAM.
+#ifndef HR_HIST_PF
+#define HR_HIST_PF 3
+#endif
+__device__ __forceinline__ void prefetch_row_l2(const uint8_t* row, size_t bytes, uintptr_t img_end) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(row) & ~(uintptr_t)15;
+  uintptr_t e = (reinterpret_cast<uintptr_t>(row) + bytes + 15) & ~(uintptr_t)15;
+  if (e > img_end) e = img_end;
+  if (e > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
+
 // Zero the counters (all NT threads; caller synchronises before use).
 template <int NT>
 __device__ __forceinline__ void hist_zero(uint32_t* sm) {
@@ -184,10 +199,12 @@ __device__ __forceinline__ void hist_zero(uint32_t* sm) {
 // halo row when `halo`), starting at p (the strip's first byte in row ya).  rowEnd: the strip's
 // last pixel is x = W - 1 (dx = 0 there, no neighbour load).  RPG + 1 row steps for every lane
 // (a warp-uniform trip count); lanes with nr == 0 only mask their counts.
+// pf: this thread prefetches its group's rows into L2, HR_HIST_PF rows ahead (p is then the
+// row start; img_end the 16-B aligned-down end of the image).
 template <int G, int VEC>
 __device__ __forceinline__ void walk_strip(const uint8_t* __restrict__ p, size_t rowBytes, int RPG, int nr,
                                            bool halo, bool rowEnd, uint32_t sb, uint32_t* ghi, uint32_t Lv,
-                                           uint32_t Lg) {
+                                           uint32_t Lg, bool pf = false, uintptr_t img_end = 0) {
   uint32_t Vp[G], Dp[G];
 #pragma unroll
   for (int q = 0; q < G; ++q) Vp[q] = Dp[q] = 0u;
@@ -237,8 +254,15 @@ __device__ __forceinline__ void walk_strip(const uint8_t* __restrict__ p, size_t
   uint32_t wa[3 * G], wb[3 * G], na = 0u, nb = 0u;
 #pragma unroll
   for (int i = 0; i < 3 * G; ++i) wa[i] = wb[i] = 0u;
+  if (pf)
+    for (int r = 1; r < HR_HIST_PF; ++r)
+      if (need(r)) prefetch_row_l2(p + r * rowBytes, rowBytes, img_end);
   if (need(0)) load_row(p, wa, na);
   for (int it = 0; it <= RPG; it += 2) {
+    if (pf) {  // rows it + PF and it + PF + 1 (this step pair's loads are rows it + 1, it + 2)
+      if (need(it + HR_HIST_PF)) prefetch_row_l2(p + HR_HIST_PF * rowBytes, rowBytes, img_end);
+      if (need(it + HR_HIST_PF + 1)) prefetch_row_l2(p + (HR_HIST_PF + 1) * rowBytes, rowBytes, img_end);
+    }
     if (need(it + 1)) load_row(p + rowBytes, wb, nb);
     step(wa, na, it);
     if (it + 1 > RPG) break;
@@ -311,7 +335,9 @@ __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, in
         const int x0 = act ? s * SW : 0;
         const bool rowEnd = (s == SPf - 1) && (xt == W) && !halfOk;  // last pixel of this strip is x = W-1
         const uint8_t* p = img + (size_t)(act ? ya : 0) * rowBytes + (size_t)x0 * 3;
-        walk_strip<G, VEC>(p, rowBytes, RPG, nr, halo, rowEnd, sb, ghi, Lv, Lg);
+        // the first strip of each row group prefetches the group's whole rows into L2
+        const uintptr_t img_end = (reinterpret_cast<uintptr_t>(img) + (size_t)H * rowBytes) & ~(uintptr_t)15;
+        walk_strip<G, VEC>(p, rowBytes, RPG, nr, halo, rowEnd, sb, ghi, Lv, Lg, act && s == 0 && HR_HIST_PF > 0, img_end);
       }
     }
   }

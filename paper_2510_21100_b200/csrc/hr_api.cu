@@ -44,6 +44,26 @@ struct hr_ctx {
                             // 0.261 -- and 90 for larger batches -- the last group's few solves
                             // overlap the first group's apply, C5 230 + 26 images 0.167 vs 0.177)
   int apply_gs = 8;         // grouped step's apply: 1024-px chunks per warp in a CTA ticket
+  int graph_b1 = 1;         // hr_enhance of one image: replay a cached CUDA graph of the step
+                            // (C1 0.0629 -> 0.0614 ms, C2 0.0777 -> 0.0757, C4 0.2063 -> 0.2048;
+                            // batches lose the PDL overlap between consecutive steps, so B >= 2
+                            // launches directly: C3 0.2490 vs 0.2507, C5 0.1625 vs 0.1643)
+  // cached single-image step graphs, keyed by every argument of the call (LRU)
+  struct GraphEntry {
+    const uint8_t* in;
+    uint8_t* out;
+    void* ws;
+    cudaStream_t st;
+    int32_t H, W;
+    hr_params p;
+    cudaGraphExec_t exec;
+    int slot;         // the index_1 table slot the graph reads
+    int64_t kernels;  // kernels one replay launches (hr_kernel_launches)
+    uint64_t used;
+  };
+  static constexpr int kGraphs = 8;
+  GraphEntry graphs[kGraphs] = {};
+  uint64_t graph_clock = 0;
   int64_t launches = 0;     // kernels launched through this context (hr_kernel_launches)
   int last_path = -1;       // hr_last_path: 0 separate kernels, 3 grouped step
   cudaStream_t sIn = nullptr, sOut = nullptr;  // hr_enhance_host copy streams
@@ -171,6 +191,11 @@ cudaError_t idx1_table(hr_ctx* c, double gamma, const uint8_t** out, int* slot) 
   const int i = c->idx1_next;
   cudaError_t e = cudaSuccess;
   if (c->idx1_valid[i]) e = cudaEventSynchronize(c->idx1_used[i]);  // in-flight readers are done
+  for (auto& g : c->graphs)  // cached step graphs that read this slot
+    if (g.exec && g.slot == i) {
+      cudaGraphExecDestroy(g.exec);
+      g = hr_ctx::GraphEntry{};
+    }
   if (e == cudaSuccess && !c->idx1_tab[i]) e = cudaMalloc(&c->idx1_tab[i], 256 * 256);
   if (e == cudaSuccess && !c->idx1_used[i]) e = cudaEventCreateWithFlags(&c->idx1_used[i], cudaEventDisableTiming);
   if (e == cudaSuccess && !c->sTab) e = cudaStreamCreateWithFlags(&c->sTab, cudaStreamNonBlocking);
@@ -249,6 +274,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   env("HR_GROUPS", c->groups, -1, 64);
   env("HR_GROUP_FIRST_PCT", c->group_first_pct, -1, 99);
   env("HR_APPLY_GS", c->apply_gs, 1, 1 << 20);
+  env("HR_GRAPH_B1", c->graph_b1, 0, 1);
   *out = c;
   return HR_OK;
 }
@@ -257,6 +283,8 @@ hr_status hr_destroy(hr_ctx* c) {
   if (c) {
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : c->hev) cudaEventDestroy(e);
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     if (c->sIn) cudaStreamDestroy(c->sIn);
     if (c->sOut) cudaStreamDestroy(c->sOut);
     for (int i = 0; i < hr_ctx::kTab; ++i) {
@@ -294,7 +322,7 @@ const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
       {"hist_cpsm", &c->hist_cpsm, 1, 2},          {"apply_cpsm", &c->apply_cpsm, 1, 2},
       {"solve_cpsm", &c->solve_cpsm, 0, 2},        {"solve_wide_px", &c->solve_wide_px, 0, 1 << 30},
       {"groups", &c->groups, -1, 64},              {"group_first_pct", &c->group_first_pct, -1, 99},
-      {"apply_gs", &c->apply_gs, 1, 1 << 20},
+      {"apply_gs", &c->apply_gs, 1, 1 << 20},      {"graph_b1", &c->graph_b1, 0, 1},
   };
   for (const Knob& k : knobs)
     if (strcmp(k.name, key) == 0) {
@@ -581,7 +609,62 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
 
 hr_status hr_enhance(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, const hr_params* p,
                      uint8_t* out, void* ws, void* stream) {
-  return hr_enhance_debug(c, in, B, H, W, p, out, ws, nullptr, stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  // one image: the step's launches (zeroing, histograms, solve, apply: launch-latency bound at
+  // these sizes) replayed from a cached CUDA graph captured from the same calls; the PDL edges
+  // become programmatic graph edges.  Not for the legacy default stream (no capture there),
+  // while stage profiling is on, or while the caller itself is capturing.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (!c || !c->graph_b1 || B != 1 || !st || st == cudaStreamLegacy || st == cudaStreamPerThread || c->prof ||
+      cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone ||
+      check_shape(c, B, H, W) != HR_OK || check_params(c, p) != HR_OK || !in || !out || !ws || in == out) {
+    cudaGetLastError();
+    return hr_enhance_debug(c, in, B, H, W, p, out, ws, nullptr, stream);
+  }
+  hr_status s = activate(c);
+  if (s) return s;
+  for (auto& g : c->graphs)
+    if (g.exec && g.in == in && g.out == out && g.ws == ws && g.st == st && g.H == H && g.W == W &&
+        memcmp(&g.p, p, sizeof(hr_params)) == 0) {
+      g.used = ++c->graph_clock;
+      cudaError_t e = cudaGraphLaunch(g.exec, st);
+      if (e == cudaSuccess) c->launches += g.kernels;
+      if (e == cudaSuccess) e = cudaEventRecord(c->idx1_used[g.slot], st);
+      return cuda_err(c, e, "hr_enhance (graph)");
+    }
+  // miss: build the gamma's index_1 table outside the capture, capture the step, instantiate
+  const uint8_t* tab = nullptr;
+  int slot = 0;
+  cudaError_t e = idx1_table(c, p->gamma, &tab, &slot);
+  if (e != cudaSuccess) return cuda_err(c, e, "hr_enhance (index_1 table)");
+  e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return hr_enhance_debug(c, in, B, H, W, p, out, ws, nullptr, stream);
+  }
+  const int64_t l0 = c->launches;
+  const hr_status r = hr_enhance_debug(c, in, B, H, W, p, out, ws, nullptr, stream);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(st, &graph);
+  const int64_t nk = c->launches - l0;
+  c->launches = l0;
+  if (r != HR_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  cudaGraphExec_t exec = nullptr;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_err(c, e, "hr_enhance (graph capture)");
+  hr_ctx::GraphEntry* v = &c->graphs[0];  // the least recently used slot
+  for (auto& g : c->graphs)
+    if (g.used < v->used) v = &g;
+  if (v->exec) cudaGraphExecDestroy(v->exec);
+  *v = hr_ctx::GraphEntry{in, out, ws, st, H, W, *p, exec, slot, nk, ++c->graph_clock};
+  e = cudaGraphLaunch(exec, st);
+  if (e == cudaSuccess) c->launches += nk;
+  if (e == cudaSuccess) e = cudaEventRecord(c->idx1_used[slot], st);
+  return cuda_err(c, e, "hr_enhance (graph)");
 }
 
 hr_status hr_he(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, uint8_t* out, uint8_t* lut_dbg,

@@ -170,3 +170,46 @@ def test_many_gammas_reuse_index1_tables():
     for g, o in list(zip(gammas, outs))[::9]:
         r = oracle.enhance(x[0].cpu().numpy(), oracle.Params(gamma=g))
         assert np.array_equal(o[0].cpu().numpy(), r.out), g
+
+
+def test_single_image_graph_replay():
+    """One image on a non-default stream: hr_enhance captures its step into a cached CUDA graph
+    and replays it; outputs equal the direct launches, a new buffer or parameter set captures
+    anew, and the kernel counter counts the replayed kernels."""
+    m = hr()
+    x = torch.from_numpy(batch(1, 90, 160, seed0=41)).cuda()
+    ref = m.hr_enhance(x)  # legacy default stream: direct launches
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        outs = []
+        out = torch.empty_like(x)
+        ws = torch.empty(m.workspace_bytes(1, 90, 160), dtype=torch.uint8, device="cuda")
+        for g in (2.2, 2.2, 1.5, 2.2):
+            k0 = m.kernel_launches()
+            m.hr_enhance(x, m.Params(gamma=g), out=out, workspace=ws)
+            outs.append((g, out.clone(), m.kernel_launches() - k0))
+        s.synchronize()
+    assert torch.equal(outs[0][1], ref) and torch.equal(outs[1][1], ref) and torch.equal(outs[3][1], ref)
+    assert outs[0][2] == outs[1][2] == outs[3][2] > 0
+    r15 = oracle.enhance(x[0].cpu().numpy(), oracle.Params(gamma=1.5))
+    assert np.array_equal(outs[2][1][0].cpu().numpy(), r15.out)
+
+
+def test_graphs_with_many_gammas():
+    """One image on a side stream with more gammas than cached index_1 tables: evicting a table
+    also drops the cached step graphs that read it; every output matches the oracle."""
+    m = hr()
+    x = torch.from_numpy(batch(1, 24, 32, seed0=6)).cuda()
+    s = torch.cuda.Stream()
+    gammas = [1.0 + 0.04 * i for i in range(70)] + [1.0, 1.04, 3.76]
+    with torch.cuda.stream(s):
+        out = torch.empty_like(x)
+        ws = torch.empty(m.workspace_bytes(1, 24, 32), dtype=torch.uint8, device="cuda")
+        res = []
+        for g in gammas:
+            m.hr_enhance(x, m.Params(gamma=g), out=out, workspace=ws)
+            res.append(out.clone())
+        s.synchronize()
+    for g, o in list(zip(gammas, res))[::7] + list(zip(gammas, res))[-3:]:
+        r = oracle.enhance(x[0].cpu().numpy(), oracle.Params(gamma=g))
+        assert np.array_equal(o[0].cpu().numpy(), r.out), g
