@@ -179,7 +179,7 @@ __device__ __forceinline__ void grad_row(uint32_t sb, uint32_t* ghi, uint32_t Lg
 // the caller's buffer.  Issued a few rows ahead of the walk by the first thread of each row
 // group: the walk's own loads (one row ahead, registers) then hit L2 instead of DRAM.
 #ifndef HR_HIST_PF
-#define HR_HIST_PF 3
+#define HR_HIST_PF 2
 #endif
 __device__ __forceinline__ void prefetch_row_l2(const uint8_t* row, size_t bytes, uintptr_t img_end) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(row) & ~(uintptr_t)15;

@@ -176,6 +176,7 @@ hr_status activate(hr_ctx* c) {
 }
 
 int hist_grid(const hr_ctx* c) { return c->hist_cpsm * c->num_sms; }
+int hist_nt(const hr_ctx* c) { return c->hist_cpsm == 1 ? 1024 : hr::kHistThreads; }  // 1 CTA/SM: 1024 threads
 int apply_grid(const hr_ctx* c) { return c->apply_cpsm * c->num_sms; }
 int solve_cpsm_for(const hr_ctx* c, int64_t B) { return c->solve_cpsm ? c->solve_cpsm : (B <= c->num_sms ? 1 : 2); }
 
@@ -410,7 +411,7 @@ hr_status hr_histogram(hr_ctx* c, const uint8_t* rgb, int64_t B, int32_t H, int3
   uint32_t* graw = hist_g_raw ? hist_g_raw : reinterpret_cast<uint32_t*>((char*)ws + L.graw);
   cudaError_t e = cudaMemsetAsync(hist_s, 0, (size_t)B * kLevels * sizeof(uint32_t), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(graw, 0, (size_t)B * kGradSlots * sizeof(uint32_t), st);
-  if (e == cudaSuccess) e = counted(c, hr::launch_hist(rgb, B, H, W, hist_s, graw, hist_grid(c), st));
+  if (e == cudaSuccess) e = counted(c, hr::launch_hist(rgb, B, H, W, hist_s, graw, hist_grid(c), st, nullptr, false, hist_nt(c)));
   if (e == cudaSuccess) e = counted(c, hr::launch_remap(graw, B, grad_norm, hist_g, st));
   return cuda_err(c, e, "hr_histogram");
 }
@@ -584,7 +585,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       const int64_t b0 = gstart(k), nb = gstart(k + 1) - b0;
       const int grid = (int)std::max<int64_t>(c->num_sms, slots - std::min<int64_t>(prev_nb, slots / 2));
       e = counted(c, hr::launch_hist(in + b0 * img, nb, H, W, hs + b0 * kLevels, graw + b0 * kGradSlots, grid, st,
-                                     done + b0, k > 0));
+                                     done + b0, k > 0, hist_nt(c)));
       if (e == cudaSuccess) e = solve_group(b0, nb, 2, true);
       prev_nb = nb;
     }
@@ -596,7 +597,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     // separate kernels: hist | solve + LUT | apply, chained by PDL; the apply grid, launched
     // early, starts on images whose LUT-ready flag is set while the solver grid finishes
     c->last_path = 0;
-    if (e == cudaSuccess) e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st));
+    if (e == cudaSuccess) e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st, nullptr, false, hist_nt(c)));
     if (e == cudaSuccess) e = mark(1);
     if (e == cudaSuccess) e = solve_group(0, B, solve_cpsm_for(c, B), false);
     if (e == cudaSuccess) e = mark(2);
@@ -682,7 +683,7 @@ hr_status hr_he(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, int32_t W, u
   uint8_t* lut = lut_dbg ? lut_dbg : reinterpret_cast<uint8_t*>((char*)ws + L.lut);
   cudaError_t e = counted(c, hr::launch_zero(hs, (size_t)B * kLevels * sizeof(uint32_t), st));
   if (e == cudaSuccess) e = counted(c, hr::launch_zero(graw, (size_t)B * kGradSlots * sizeof(uint32_t), st));
-  if (e == cudaSuccess) e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st));
+  if (e == cudaSuccess) e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st, nullptr, false, hist_nt(c)));
   if (e == cudaSuccess) e = counted(c, hr::launch_he_lut(hs, B, lut, st));
   if (e == cudaSuccess) e = counted(c, hr::launch_apply(in, lut, B, H, W, out, apply_grid(c), st));
   return cuda_err(c, e, "hr_he");

@@ -162,7 +162,7 @@ cudaError_t init_attrs_apply();
 // solver of group k - 1)
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
                         uint32_t* hist_graw, int grid, cudaStream_t st, uint32_t* done = nullptr,
-                        bool nowait = false);
+                        bool nowait = false, int nt = kHistThreads);
 int hist_grid_clamped(int64_t B, int32_t H, int grid);  // the grid launch_hist actually uses
 cudaError_t launch_remap(const uint32_t* hist_graw, int64_t B, int32_t grad_norm, uint32_t* hist_g,
                          cudaStream_t st);

@@ -51,7 +51,10 @@ k_hist(const uint8_t* __restrict__ rgb, int64_t B, int H, int W, uint32_t* __res
 
 template <int SW, int VEC>
 cudaError_t launch_v(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hs, uint32_t* hg, int grid,
-                     uint32_t* done, cudaStream_t st, bool nowait) {
+                     uint32_t* done, cudaStream_t st, bool nowait, int nt) {
+  if (nt == 1024)
+    return launch_pdl(k_hist<SW, VEC, 1024>, dim3(grid), dim3(1024), kHistDevSmem, st, rgb, B, H, W, hs, hg, done,
+                      (int)nowait);
   return launch_pdl(k_hist<SW, VEC, kHistThreads>, dim3(grid), dim3(kHistThreads), kHistDevSmem, st, rgb, B, H, W,
                     hs, hg, done, (int)nowait);
 }
@@ -83,22 +86,23 @@ int hist_grid_clamped(int64_t B, int32_t H, int grid) {
 cudaError_t init_attrs_hist() {
   cudaError_t e = cudaSuccess;
   for (auto k : {k_hist<16, 16, kHistThreads>, k_hist<16, 9, kHistThreads>, k_hist<8, 8, kHistThreads>,
-                 k_hist<16, 1, kHistThreads>})
+                 k_hist<16, 1, kHistThreads>, k_hist<16, 16, 1024>, k_hist<16, 9, 1024>, k_hist<8, 8, 1024>,
+                 k_hist<16, 1, 1024>})
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistDevSmem);
   return e;
 }
 
 cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uint32_t* hist_s,
-                        uint32_t* hist_graw, int grid, cudaStream_t st, uint32_t* done, bool nowait) {
+                        uint32_t* hist_graw, int grid, cudaStream_t st, uint32_t* done, bool nowait, int nt) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(rgb);
   grid = hist_grid_clamped(B, H, grid);
-  if (a % 16 == 0 && W % 16 == 0) return launch_v<16, 16>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait);
+  if (a % 16 == 0 && W % 16 == 0) return launch_v<16, 16>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait, nt);
   // 8-B aligned rows, W % 16 == 8: 16-px strips with mixed 16-B / 8-B loads by row parity and
   // half-strip walkers for the last 8 columns; other W % 8 == 0: 8-px strips
   if (a % 8 == 0 && W % 8 == 0 && W >= 16)
-    return launch_v<16, 9>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait);
-  if (a % 8 == 0 && W % 8 == 0) return launch_v<8, 8>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait);
-  return launch_v<16, 1>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait);
+    return launch_v<16, 9>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait, nt);
+  if (a % 8 == 0 && W % 8 == 0) return launch_v<8, 8>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait, nt);
+  return launch_v<16, 1>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait, nt);
 }
 
 }  // namespace hr

@@ -1,13 +1,9 @@
-# A/B over arbitrary environment settings on bench configs (run with gpurun from the repo root):
-#   bash tools/ab_env.sh "C3 C5" "A=1 B=2" "A=0" ...      (each quoted group is one setting)
-mkdir -p gpurun_out
-CFGS=$1; shift
-for c in $CFGS; do
-  i=0
-  for setting in "$@"; do
-    i=$((i+1))
-    env $setting python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/abe_${c}_$i.json 2>gpurun_out/abe_${c}_$i.err
-    python -c "
-import json; d=json.load(open('gpurun_out/abe_${c}_$i.json')); s=d['stages_ms']; print('$c [$setting]', d['ms_per_step'], d['hbm_roofline_frac_e2e'], 'hist', s['hist'], 'solve', s['solve'], 'apply', s['apply'])" || tail -3 gpurun_out/abe_${c}_$i.err
+# A/B of environment settings (policy knobs HR_<KEY>) on bench configs (gpurun, repo root):
+#   bash tools/ab_env.sh "C5 C3" "" "HR_HIST_CPSM=1" ...   ("" = defaults)
+cfgs=$1; shift
+for c in $cfgs; do
+  for envs in "$@"; do
+    r=$(env $envs python bench.py --config $c --steps 200 --warmup 5 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1)
+    echo "$c [$envs] $(echo "$r" | python -c "import json,sys; d=json.loads(sys.stdin.read()); t=d['timing']; s=d['stages_ms_separate_kernels_info']; print(d['ms_per_step'], 'p50', t['median_ms'], 'hist', s['hist'], 'apply', s['apply'], 'solve', s['solve'])")"
   done
 done
