@@ -258,6 +258,11 @@ hr_status hr_trace_bind(hr_ctx* ctx, void* records_dev, uint32_t* count_dev, uin
                     group's few solves beside the first group's apply, C5 0.167 vs 0.177)
      "apply_gs"     grouped step's apply: 1024-pixel chunks per warp in one CTA  default 8
                     ticket of the last group (>= 1)
+     "solve_cluster" images of H*W >= solve_wide_px (<= 9 per call, separate   default 1
+                    kernels): each solved by a thread-block cluster exchanging
+                    partial sums through distributed shared memory: 1 = 8 CTAs x
+                    256 threads, 2 = 8 x 512, 3 = 16 x 256, 4 = 16 x 512; 0: one
+                    512-thread CTA (C4: 77 us vs 119 us per image)
      "graph_b1"     hr_enhance with B == 1 on a non-default stream: the step is     default 1
                     captured once into a CUDA graph (cached per call arguments,
                     8 entries, LRU) and replayed (C1/C2/C4 1.5-2 us faster; batches

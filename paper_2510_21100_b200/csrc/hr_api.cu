@@ -44,6 +44,10 @@ struct hr_ctx {
                             // 0.261 -- and 90 for larger batches -- the last group's few solves
                             // overlap the first group's apply, C5 230 + 26 images 0.167 vs 0.177)
   int apply_gs = 8;         // grouped step's apply: 1024-px chunks per warp in a CTA ticket
+  int solve_cluster = 1;    // large images (H*W >= solve_wide_px, <= 9 per launch, separate kernels):
+                            // one cluster per image (solve_cluster_dev.cuh): 1 = 8 CTAs x 256
+                            // threads (C4 solve 119 -> 77 us), 2 = 8 x 512 (88), 3 = 16 x 256
+                            // (88), 4 = 16 x 512 (113); 0: one 512-thread CTA
   int graph_b1 = 1;         // hr_enhance of one image: replay a cached CUDA graph of the step
                             // (C1 0.0629 -> 0.0614 ms, C2 0.0777 -> 0.0757, C4 0.2063 -> 0.2048;
                             // batches lose the PDL overlap between consecutive steps, so B >= 2
@@ -276,6 +280,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   env("HR_GROUP_FIRST_PCT", c->group_first_pct, -1, 99);
   env("HR_APPLY_GS", c->apply_gs, 1, 1 << 20);
   env("HR_GRAPH_B1", c->graph_b1, 0, 1);
+  env("HR_SOLVE_CLUSTER", c->solve_cluster, 0, 4);
   *out = c;
   return HR_OK;
 }
@@ -324,6 +329,7 @@ const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
       {"solve_cpsm", &c->solve_cpsm, 0, 2},        {"solve_wide_px", &c->solve_wide_px, 0, 1 << 30},
       {"groups", &c->groups, -1, 64},              {"group_first_pct", &c->group_first_pct, -1, 99},
       {"apply_gs", &c->apply_gs, 1, 1 << 20},      {"graph_b1", &c->graph_b1, 0, 1},
+      {"solve_cluster", &c->solve_cluster, 0, 4},
   };
   for (const Knob& k : knobs)
     if (strcmp(k.name, key) == 0) {
@@ -547,6 +553,8 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     // 512-thread solver CTAs for large images (their supports, and so the cell loops, tend to be
     // large: C4 33 MP 8,480 cells; C2 0.66 MP 1,334 cells)
     const bool wide = c->solve_wide_px > 0 && (int64_t)H * W >= c->solve_wide_px;
+    if (wide && c->solve_cluster && nb <= hr::kClusterMaxB && !wait_done)
+      return counted(c, hr::launch_solve_cluster(a, nb, st, c->solve_cluster));
     return counted(c, hr::launch_solve(a, nb, cpsm, st, wide));
   };
   auto zero = [&](void* q, size_t n) -> cudaError_t { return counted(c, hr::launch_zero(q, n, st)); };

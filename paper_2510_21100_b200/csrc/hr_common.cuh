@@ -195,6 +195,11 @@ cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st);
 // 121 us per image; small ones are faster at 256 threads: C2 37 vs 43 us)
 cudaError_t launch_solve(const SolveArgs& a, int64_t B, int cpsm, cudaStream_t st, bool wide = false);
 size_t solve_smem_bytes(int arena_bytes = 0);
+// the cluster solver (one image per cluster of kClusterCS CTAs; large single images)
+constexpr int kClusterCS = 16;   // largest cluster (ranks with their own global arenas)
+constexpr int kClusterMaxB = 9;  // images per cluster launch (148 SMs / 16)
+// variant: 1 = 8 CTAs x 256 threads, 2 = 8 x 512, 3 = 16 x 256, 4 = 16 x 512
+cudaError_t launch_solve_cluster(const SolveArgs& a, int64_t B, cudaStream_t st, int variant);
 size_t solve_cells_ws_bytes(int64_t B);
 
 cudaError_t launch_match(const uint32_t* hist_s, const double* target, int64_t B, uint8_t* lut,

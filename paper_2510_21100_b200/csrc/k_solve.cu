@@ -6,7 +6,7 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include "solve_dev.cuh"
+#include "solve_cluster_dev.cuh"
 
 namespace hr {
 namespace {
@@ -38,6 +38,27 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_solve(SolveArgs args) {
     if (threadIdx.x == 0) st_release(args.ready + b, 1u);
   }
   TRACE_END(3u, (uint32_t)((uintptr_t)args.hist_s >> 8), tr_mid);  // aux: which launch (group)
+}
+
+// One image per cluster of CS CTAs (solve_cluster_dev.cuh): large single images.
+template <int NT, int CS>
+__global__ void __launch_bounds__(NT, 1) k_solve_cluster(SolveArgs args) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ int wscr[NT / 32];
+  TRACE_T0();
+  unsigned long long tr_mid = 0ull;
+  (void)tr_mid;
+  pdl_wait();
+  pdl_trigger();
+  const int64_t b = blockIdx.x / CS;
+  TRACE_MID(tr_mid);
+  solve_image_cluster<NT, CS>(args, b, smraw, wscr);
+  if (args.ready && (blockIdx.x % CS) == 0) {  // rank 0 wrote the LUT
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(args.ready + b, 1u);
+  }
+  TRACE_END(3u, (uint32_t)((uintptr_t)args.hist_s >> 8), tr_mid);
 }
 
 // index_1(i, j) of Eqs. 17-19 for every (i, j), once per gamma (R4, R5):
@@ -77,7 +98,19 @@ __global__ void __launch_bounds__(kLevels) k_match(const uint32_t* hist_s, const
 cudaError_t trace_bind_solve(void* buf, uint32_t* n, uint32_t cap) { return trace_bind_tu(buf, n, cap); }
 
 size_t solve_smem_bytes(int arena_bytes) { return sizeof(Sm) + (size_t)(arena_bytes > 0 ? arena_bytes : kArenaSmem); }
-size_t solve_cells_ws_bytes(int64_t B) { return (size_t)B * (size_t)kArenaGlobal; }
+// one global arena per image, or per (image, rank) when the image may take the cluster solver
+size_t solve_cells_ws_bytes(int64_t B) {
+  return (size_t)std::max<int64_t>(B, std::min<int64_t>(B, kClusterMaxB) * kClusterCS) * (size_t)kArenaGlobal;
+}
+size_t solve_cluster_smem_bytes() { return sizeof(Sm) + sizeof(SmClusterExtra) + (size_t)kArenaSmem; }
+
+template <int NT, int CS>
+cudaError_t cluster_attrs() {
+  cudaError_t e = cudaFuncSetAttribute(k_solve_cluster<NT, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)solve_cluster_smem_bytes());
+  if (e == cudaSuccess && CS > 8) e = cudaFuncSetAttribute(k_solve_cluster<NT, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return e;
+}
 
 constexpr int kBigArena = 190 * 1024;  // sizeof(Sm) + 190 KB <= 227 KB per block
 
@@ -89,6 +122,10 @@ cudaError_t init_attrs_solve() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
   }
+  if (e == cudaSuccess) e = cluster_attrs<256, 8>();
+  if (e == cudaSuccess) e = cluster_attrs<512, 8>();
+  if (e == cudaSuccess) e = cluster_attrs<256, 16>();
+  if (e == cudaSuccess) e = cluster_attrs<512, 16>();
   return e;
 }
 
@@ -102,6 +139,37 @@ cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t 
   if (cpsm == 1 && wide)
     return launch_pdl(k_solve<512>, dim3((unsigned)B), dim3(512), solve_smem_bytes(a.arena_bytes), st, a);
   return launch_pdl(k_solve<256>, dim3((unsigned)B), dim3(256), solve_smem_bytes(a.arena_bytes), st, a);
+}
+
+// B images, one cluster of kClusterCS CTAs (256 threads each) per image (B <= kClusterMaxB)
+template <int NT, int CS>
+cudaError_t launch_cluster_v(const SolveArgs& a0, int64_t B, cudaStream_t st) {
+  SolveArgs a = a0;
+  a.arena_bytes = kArenaSmem;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(B * CS));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = solve_cluster_smem_bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k_solve_cluster<NT, CS>, a);
+}
+
+cudaError_t launch_solve_cluster(const SolveArgs& a, int64_t B, cudaStream_t st, int variant) {
+  switch (variant) {
+    case 2: return launch_cluster_v<512, 8>(a, B, st);
+    case 3: return launch_cluster_v<256, 16>(a, B, st);
+    case 4: return launch_cluster_v<512, 16>(a, B, st);
+    default: return launch_cluster_v<256, 8>(a, B, st);
+  }
 }
 
 cudaError_t launch_idx1_table(double gamma, uint8_t* tab, cudaStream_t st) {

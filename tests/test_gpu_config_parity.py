@@ -138,3 +138,52 @@ def test_dense_supports_fp64(groups):
     assert max(errs) <= RTOL
     assert np.array_equal(r["lut"].cpu().numpy().astype(np.int32), ref["lut"])
     assert np.array_equal(r["out"].cpu().numpy(), ref["out"])
+
+
+def test_c4_single_cta_512_thread_solver():
+    run_config("C4", solve_cluster=0)
+
+
+def _check_full(x, **policy):
+    m = hr()
+    saved = [(k, m.get_policy(k)) for k in policy]
+    for k, v in policy.items():
+        m.set_policy(k, v)
+    try:
+        r = m.hr_enhance_debug(torch.from_numpy(x).cuda(), m.Params(), full=True)
+        torch.cuda.synchronize()
+    finally:
+        for k, v in saved:
+            m.set_policy(k, v)
+    ref = oracle.enhance_batch(x, oracle.Params(), nthreads=NTHREADS, want_out=True)
+    assert np.array_equal(r["hist_s"].cpu().numpy().astype(np.uint64), ref["hS"])
+    assert np.array_equal(r["hist_g"].cpu().numpy().astype(np.uint64), ref["hG"])
+    assert np.array_equal(r["iters"].cpu().numpy(), ref["iters"])
+    errs = [rel_err(r[k].cpu().numpy(), ref[k2]) for k, k2 in (("hL", "hL"), ("hR", "hR"), ("target", "T"))]
+    assert max(errs) <= RTOL, errs
+    assert np.array_equal(r["lut"].cpu().numpy().astype(np.int32), ref["lut"])
+    assert np.array_equal(r["out"].cpu().numpy(), ref["out"])
+    return errs
+
+
+@pytest.mark.parametrize("case", ["constant", "two_levels", "noise", "pair", "dark"])
+def test_cluster_solver_cases(case):
+    """Large images (>= solve_wide_px) take the cluster solver (8 CTAs, DSMEM exchange): fewer
+    gradient levels than ranks (ranks without rows), dense supports (per-rank global arenas),
+    two images (two clusters), a dark image; each against the oracle in both solvers."""
+    H, W = 2048, 2048
+    rng = np.random.default_rng(3)
+    if case == "constant":
+        x = np.full((1, H, W, 3), (90, 40, 10), np.uint8)
+    elif case == "two_levels":
+        x = np.zeros((1, H, W, 3), np.uint8)
+        x[0, :, W // 2:] = 200
+    elif case == "noise":
+        x = rng.integers(0, 256, size=(1, H, W, 3), dtype=np.uint8)
+    elif case == "pair":
+        x = np.stack([synth.make_image(H, W, seed=71, peak=0.2), synth.make_image(H, W, seed=72, peak=0.05)])
+    else:
+        x = synth.make_image(H, W, seed=73, peak=0.03)[None]
+    e1 = _check_full(x, groups=0)
+    e2 = _check_full(x, groups=0, solve_cluster=0)
+    print(f"{case}: max rel err cluster {max(e1):.2e}, single CTA {max(e2):.2e}")
