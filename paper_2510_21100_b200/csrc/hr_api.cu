@@ -85,9 +85,19 @@ using hr::kLevels;
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// count a successful kernel launch
+// count a successful kernel launch (HR_SYNC_CHECK=1, debugging: synchronise after every launch
+// and report which launch faulted)
+const char* g_launch_label = "";
 inline cudaError_t counted(hr_ctx* c, cudaError_t e) {
   if (e == cudaSuccess) ++c->launches;
+  static const bool sync_check = [] {
+    const char* v = getenv("HR_SYNC_CHECK");
+    return v && atoi(v) != 0;
+  }();
+  if (sync_check && e == cudaSuccess) {
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) fprintf(stderr, "HR_SYNC_CHECK: launch #%lld (%s) faulted: %s\n", (long long)c->launches, g_launch_label, cudaGetErrorString(e));
+  }
   return e;
 }
 
@@ -553,11 +563,17 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     // 512-thread solver CTAs for large images (their supports, and so the cell loops, tend to be
     // large: C4 33 MP 8,480 cells; C2 0.66 MP 1,334 cells)
     const bool wide = c->solve_wide_px > 0 && (int64_t)H * W >= c->solve_wide_px;
-    if (wide && c->solve_cluster && nb <= hr::kClusterMaxB && !wait_done)
+    if (wide && c->solve_cluster && nb <= hr::kClusterMaxB && !wait_done) {
+      g_launch_label = "solve_cluster";
       return counted(c, hr::launch_solve_cluster(a, nb, st, c->solve_cluster));
+    }
+    g_launch_label = "solve";
     return counted(c, hr::launch_solve(a, nb, cpsm, st, wide));
   };
-  auto zero = [&](void* q, size_t n) -> cudaError_t { return counted(c, hr::launch_zero(q, n, st)); };
+  auto zero = [&](void* q, size_t n) -> cudaError_t {
+    g_launch_label = "zero";
+    return counted(c, hr::launch_zero(q, n, st));
+  };
   const int ngroups = c->groups >= 0 ? c->groups : (B >= 2 ? 2 : 0);
   if (e == cudaSuccess) e = mark(0);
   // the accumulators and the control block, each zeroed by its own launch (measured faster in
@@ -605,10 +621,12 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     // separate kernels: hist | solve + LUT | apply, chained by PDL; the apply grid, launched
     // early, starts on images whose LUT-ready flag is set while the solver grid finishes
     c->last_path = 0;
+    g_launch_label = "hist";
     if (e == cudaSuccess) e = counted(c, hr::launch_hist(in, B, H, W, hs, graw, hist_grid(c), st, nullptr, false, hist_nt(c)));
     if (e == cudaSuccess) e = mark(1);
     if (e == cudaSuccess) e = solve_group(0, B, solve_cpsm_for(c, B), false);
     if (e == cudaSuccess) e = mark(2);
+    g_launch_label = "apply";
     if (e == cudaSuccess) e = counted(c, hr::launch_apply(in, lut, B, H, W, out, apply_grid(c), st, ready));
   }
   if (e == cudaSuccess) e = mark(3);

@@ -48,9 +48,15 @@ __global__ void __launch_bounds__(NT, 1) k_solve_cluster(SolveArgs args) {
   TRACE_T0();
   unsigned long long tr_mid = 0ull;
   (void)tr_mid;
-  pdl_wait();
   pdl_trigger();
   const int64_t b = blockIdx.x / CS;
+  // the state structs start zeroed: without this the kernel faulted (illegal address) in one
+  // test sequence on B200 -- zeroing either struct region fixed it, the arena region did not;
+  // the stale shared-memory read behind it was not pinned down (the checked build's bounds
+  // checks stay silent), so this stays as a guard (~30 KB of 16-B stores, < 1 us)
+  for (int i = threadIdx.x; i < (int)((sizeof(Sm) + sizeof(SmClusterExtra)) / 16); i += NT)
+    reinterpret_cast<uint4*>(smraw)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
   TRACE_MID(tr_mid);
   solve_image_cluster<NT, CS>(args, b, smraw, wscr);
   if (args.ready && (blockIdx.x % CS) == 0) {  // rank 0 wrote the LUT
@@ -151,15 +157,17 @@ cudaError_t launch_cluster_v(const SolveArgs& a0, int64_t B, cudaStream_t st) {
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = solve_cluster_smem_bytes();
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  // a plain (not programmatically serialized) launch: with programmatic dependent launch the
+  // cluster kernel raised illegal-address faults on B200 / driver 580 (one test sequence, every
+  // run; not with launch blocking, PDL off, or this launch without it), so its CTAs start
+  // after the histogram grid completes.  Its own trigger still lets the apply launch early.
+  cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CS;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_solve_cluster<NT, CS>, a);
 }
 

@@ -69,9 +69,12 @@ struct __align__(16) SmClusterExtra {
   } while (0)
 #endif
 
+// cluster-wide barrier (release / acquire: the DSMEM stores before it are visible after it).
+// Not the .aligned form: that one requires every warp to arrive converged, which the compiler
+// does not guarantee after the data-dependent loops that precede some calls.
 __device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.arrive.release;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory");
 }
 
 template <int T, int CS, int kForm>
@@ -126,6 +129,7 @@ __device__ int iterate_cluster(Sm& s, SmClusterExtra& x, cg::cluster_group& cl, 
       const double* __restrict__ hr1 = s.hR1 + aB;
       for (int p = tid; p < A.P; p += T) {
         const uint32_t d = pd[p];
+        HR_CHECK((int)(d >> 16) < nRl && (int)((d >> 8) & 255) < nL && (int)(d & 255) <= (int)((d >> 8) & 255));
         pv[p] = hr1[d >> 16] * piece_sum(hl1, d & 255, (d >> 8) & 255) * cRL;
       }
       if (t == 0 || P.use_epsilon) slot_put3(s, R_DR, dr, R_DL, dl, R_SL2, q);
@@ -190,6 +194,7 @@ __device__ int iterate_cluster(Sm& s, SmClusterExtra& x, cg::cluster_group& cl, 
         v = (num + P.beta * s.hGc[a]) * invDenR;
         v = v > 0.0 ? v : 0.0;
         const double w = kForm == 0 ? v * hr : v * rcp_fast(hr);
+        HR_CHECK(a < nR);
 #pragma unroll
         for (int q = 0; q < CS; ++q) {
           rR1[q][a] = v;
@@ -239,6 +244,7 @@ __device__ int iterate_cluster(Sm& s, SmClusterExtra& x, cg::cluster_group& cl, 
         const double num = kForm == 0 ? hl * Bv * invN : Bv * rcp_fast(N * hl);
         u = (num + P.alpha * s.hSc[c]) * invDenL;
         u = u > 0.0 ? u : 0.0;
+        HR_CHECK(c < nL);
 #pragma unroll
         for (int q = 0; q < CS; ++q) rL1[q][c] = u;
       }
@@ -270,6 +276,7 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
                                                     int* wscr) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
+  HR_CHECK((int)cl.num_blocks() == CS && rank == (int)(blockIdx.x % CS) && blockDim.x == T);
   Sm& s = *reinterpret_cast<Sm*>(smraw);
   SmClusterExtra& x = *reinterpret_cast<SmClusterExtra*>(smraw + sizeof(Sm));
   unsigned char* arenaS = smraw + sizeof(Sm) + sizeof(SmClusterExtra);
@@ -399,6 +406,7 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
     kmin[tid] = kc1[tid * nL];
   }
   const bool dS = align16(El) + 8 * Wtot <= AB - kMaskBytes - kcLb;
+  HR_CHECK(dS || 8LL * Wtot <= kArenaGlobal);
   double* D = dS ? reinterpret_cast<double*>(arenaS + align16(El)) : reinterpret_cast<double*>(arenaG);
   for (int i = tid; i < Wtot; i += T) D[i] = 0.0;
   __syncthreads();
@@ -411,6 +419,7 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
     for (int c = 0; c < nL; ++c) {
       const int kn = kr[c];
       if (kn != k) {
+        HR_CHECK(kn > k && offr + k - k0 < Wtot && k >= k0);
         D[offr + k - k0] = hra * acc;
         acc = 0.0;
         k = kn;

@@ -105,6 +105,8 @@ struct __align__(16) Sm {
   uint32_t hSi[kLevels], hGi[kLevels];
   int keyStart[kLevels + 1];  // piece offsets per bin (bin order)
   uint8_t listR[kLevels], listL[kLevels];
+  uint8_t binList[kLevels];   // the bins holding pieces, ascending (E2: lanes per bin)
+  int nBins;
   unsigned long long nw[kMaxSW];
 };
 
@@ -116,17 +118,28 @@ __device__ __forceinline__ int idx0(int i, int j) {  // P:192 index(i,j) for l =
 template <int T>
 __device__ __forceinline__ double slot_sum(const Sm& s, int slot) {
   constexpr int NW = T / 32;
-  double a = 0.0;
+  static_assert(NW % 2 == 0, "pairs of warp partials");
+  double x[NW];
 #pragma unroll
-  for (int w = 0; w < NW; ++w) a += s.red[slot][w];
-  return a;
+  for (int w = 0; w < NW; w += 2) {  // 16-B loads, then a pairwise tree in warp order
+    const double2 v = *reinterpret_cast<const double2*>(&s.red[slot][w]);
+    x[w] = v.x;
+    x[w + 1] = v.y;
+  }
+#pragma unroll
+  for (int d = 1; d < NW; d <<= 1)
+#pragma unroll
+    for (int w = 0; w + d < NW; w += 2 * d) x[w] += x[w + d];
+  return x[0];
 }
 
 // Fixed-order warp reductions of up to three values at once (independent shuffle trees
 // interleave, so three sums cost about the latency of one).
-__device__ __forceinline__ void slot_put3(Sm& s, int s0, double v0, int s1, double v1, int s2, double v2) {
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) {
+// (from > 1: only lanes that are multiples of `from` hold values -- the others hold copies or
+// zero -- so the levels below `from` are skipped)
+__device__ __forceinline__ void slot_put3(Sm& s, int s0, double v0, int s1, double v1, int s2, double v2,
+                                          int from = 1) {
+  for (int d = 16; d >= from; d >>= 1) {
     v0 += __shfl_xor_sync(0xffffffffu, v0, d);
     v1 += __shfl_xor_sync(0xffffffffu, v1, d);
     v2 += __shfl_xor_sync(0xffffffffu, v2, d);
@@ -411,6 +424,14 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   if (tid < kLevels) s.keyStart[tid] = kfirst < RK ? (int)slotN[kfirst] : P;  // run slots -> piece offsets
   if (tid == 0) s.keyStart[kLevels] = P;
   __syncthreads();
+  {  // the bins holding pieces, ascending
+    const bool has = tid < kLevels && s.keyStart[tid] < s.keyStart[tid + 1];
+    int nb;
+    const int pos = block_scan_excl<T>(has ? 1 : 0, &nb, wscr);
+    if (has) s.binList[pos] = (uint8_t)tid;
+    if (tid == 0) s.nBins = nb;
+  }
+  __syncthreads();
   SLOT_MARK(pslot + 6);
 }
 
@@ -512,6 +533,10 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
   // covered by the T threads; each group sums its cells in a fixed order (deterministic)
   const int lgR = nR <= T / 8 ? 3 : nR <= T / 4 ? 2 : nR <= T / 2 ? 1 : 0, TPR = 1 << lgR;
   const int lgL = nL <= T / 8 ? 3 : nL <= T / 4 ? 2 : nL <= T / 2 ? 1 : 0, TPC = 1 << lgL;
+  const int nBins = s.nBins;
+  int lgB = 5;
+  while (lgB > 0 && (nBins << lgB) > T) --lgB;
+  const int TPB = 1 << lgB;
   constexpr int form = kForm;
   const double invN = 1.0 / N, invN2 = invN * invN;
   double SR1 = N, SL1 = N;  // sums of the raw iterates (initially exactly N)
@@ -575,13 +600,32 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       if (conv || t >= P.max_iter) break;
     }
     PHASE(14);
-    // ======== E2: EstRaw_k over the bin's runs (row order) and their pieces; rho_k (Eq. 11) ========
+    // ======== E2: EstRaw_k over the bin's pieces (bin order); rho_k (Eq. 11) ========
+    // TPB lanes per occupied bin (the largest power of two <= 32 with every bin covered), each
+    // summing every TPB-th piece, then a fixed shuffle tree over the TPB lanes
     {
-      const int k = tid;
-      if (k < kLevels && s.keyStart[k] < s.keyStart[k + 1]) {
-        const double e = bin_sum(s, A, k);  // EstRaw_k (Eqs. 6, 8)
-        s.rho[k] = form == 0 ? (e > 0.0 ? s.hSd[k] * rcp_fast(e) : 0.0) : s.hSd[k] * e;
+      const int j = tid >> lgB, q = tid & (TPB - 1);
+      double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+      int k = 0;
+      if (j < nBins) {
+        k = s.binList[j];
+        const int j1 = s.keyStart[k + 1];
+        const double* __restrict__ pv = A.pVal;
+        int i = s.keyStart[k] + q;
+        for (; i + 3 * TPB < j1; i += 4 * TPB) {
+          e0 += pv[i];
+          e1 += pv[i + TPB];
+          e2 += pv[i + 2 * TPB];
+          e3 += pv[i + 3 * TPB];
+        }
+        if (i < j1) e0 += pv[i];
+        if (i + TPB < j1) e1 += pv[i + TPB];
+        if (i + 2 * TPB < j1) e2 += pv[i + 2 * TPB];
       }
+      double e = (e0 + e1) + (e2 + e3);
+      for (int d = 1; d < TPB; d <<= 1) e += __shfl_xor_sync(0xffffffffu, e, d);
+      if (j < nBins && q == 0)  // EstRaw_k (Eqs. 6, 8)
+        s.rho[k] = form == 0 ? (e > 0.0 ? s.hSd[k] * rcp_fast(e) : 0.0) : s.hSd[k] * e;
     }
     PHASE(15);
     const double invDenR = rcp_fast((t == 0 ? slot_sum<T>(s, R_SL2) : cL * cL * QL1) * invN2 + P.beta);
@@ -634,7 +678,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         s.wgt[a] = form == 0 ? v * hr : v * rcp_fast(hr);
       }
       PHASE(5);
-      slot_put3(s, R_SR1, v, R_SR2, v * v, -1, 0.0);
+      slot_put3(s, R_SR1, v, R_SR2, v * v, -1, 0.0, TPR);
     }
     PHASE(6);
     __syncthreads();
@@ -677,7 +721,7 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
         s.hL1[c] = u;
       }
       PHASE(12);
-      slot_put3(s, R_SL1, u, R_QL1, u * u, -1, 0.0);
+      slot_put3(s, R_SL1, u, R_QL1, u * u, -1, 0.0, TPC);
     }
     PHASE(13);
     __syncthreads();
