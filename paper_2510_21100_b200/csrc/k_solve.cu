@@ -11,9 +11,11 @@
 namespace hr {
 namespace {
 
-// NT = 256: two CTAs per SM (batches); NT = 512: one CTA per SM, the cell loops over 16 warps
-template <int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) k_solve(SolveArgs args) {
+// NT = 256: two CTAs per SM (batches); NT = 512: one CTA per SM, the cell loops over 16 warps.
+// (A 64-register form, MINB = 4 -- four per SM, two beside a histogram CTA -- measured slower on
+// C5 in the grouped step, 0.177 vs 0.165 ms, and is not built.)
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_solve(SolveArgs args) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ int wscr[NT / 32];
   TRACE_T0();
@@ -122,7 +124,7 @@ constexpr int kBigArena = 190 * 1024;  // sizeof(Sm) + 190 KB <= 227 KB per bloc
 
 cudaError_t init_attrs_solve() {
   cudaError_t e = cudaSuccess;
-  for (auto k : {k_solve<256>, k_solve<512>}) {
+  for (auto k : {k_solve<256, 2>, k_solve<512, 1>}) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem_bytes(kBigArena));
     if (e == cudaSuccess)
@@ -143,8 +145,8 @@ cudaError_t launch_solve(const SolveArgs& a0, int64_t B, int cpsm, cudaStream_t 
   SolveArgs a = a0;
   if (cpsm == 1 && a.arena_bytes == 0) a.arena_bytes = kBigArena;
   if (cpsm == 1 && wide)
-    return launch_pdl(k_solve<512>, dim3((unsigned)B), dim3(512), solve_smem_bytes(a.arena_bytes), st, a);
-  return launch_pdl(k_solve<256>, dim3((unsigned)B), dim3(256), solve_smem_bytes(a.arena_bytes), st, a);
+    return launch_pdl(k_solve<512, 1>, dim3((unsigned)B), dim3(512), solve_smem_bytes(a.arena_bytes), st, a);
+  return launch_pdl(k_solve<256, 2>, dim3((unsigned)B), dim3(256), solve_smem_bytes(a.arena_bytes), st, a);
 }
 
 // B images, one cluster of kClusterCS CTAs (256 threads each) per image (B <= kClusterMaxB)
