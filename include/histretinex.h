@@ -258,6 +258,11 @@ hr_status hr_trace_bind(hr_ctx* ctx, void* records_dev, uint32_t* count_dev, uin
                     group's few solves beside the first group's apply, C5 0.167 vs 0.177)
      "apply_gs"     grouped step's apply: 1024-pixel chunks per warp in one CTA  default 8
                     ticket of the last group (>= 1)
+     "apply_full_grid" grouped step's apply grid: 1 every slot (2 per SM; CTAs  default -1
+                    that start once the last solver CTAs leave add capacity), 0 the
+                    slots the last group's solver CTAs leave, -1 auto = every slot
+                    when the last group is the larger (C3 0.2407 vs 0.2509 ms; C5,
+                    a 90% first group, keeps the reduced grid: 0.1649 vs 0.1876)
      "solve_cluster" images of H*W >= solve_wide_px (<= 9 per call, separate   default 1
                     kernels): each solved by a thread-block cluster exchanging
                     partial sums through distributed shared memory: 1 = 8 CTAs x

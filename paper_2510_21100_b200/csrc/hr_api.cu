@@ -44,6 +44,8 @@ struct hr_ctx {
                             // 0.261 -- and 90 for larger batches -- the last group's few solves
                             // overlap the first group's apply, C5 230 + 26 images 0.167 vs 0.177)
   int apply_gs = 8;         // grouped step's apply: 1024-px chunks per warp in a CTA ticket
+  int apply_full_grid = -1; // grouped step's apply grid: 1 every slot, 0 the slots the last group's
+                            // solvers leave, -1 auto (every slot when the last group is the larger)
   int solve_cluster = 1;    // large images (H*W >= solve_wide_px, <= 9 per launch, separate kernels):
                             // one cluster per image (solve_cluster_dev.cuh): 1 = 8 CTAs x 256
                             // threads (C4 solve 119 -> 77 us), 2 = 8 x 512 (88), 3 = 16 x 256
@@ -289,6 +291,7 @@ hr_status hr_create(hr_ctx** out, int device) {
   env("HR_GROUPS", c->groups, -1, 64);
   env("HR_GROUP_FIRST_PCT", c->group_first_pct, -1, 99);
   env("HR_APPLY_GS", c->apply_gs, 1, 1 << 20);
+  env("HR_APPLY_FULL_GRID", c->apply_full_grid, -1, 1);
   env("HR_GRAPH_B1", c->graph_b1, 0, 1);
   env("HR_SOLVE_CLUSTER", c->solve_cluster, 0, 4);
   *out = c;
@@ -339,6 +342,7 @@ const Knob* find_knob(hr_ctx* c, const char* key, Knob* out) {
       {"solve_cpsm", &c->solve_cpsm, 0, 2},        {"solve_wide_px", &c->solve_wide_px, 0, 1 << 30},
       {"groups", &c->groups, -1, 64},              {"group_first_pct", &c->group_first_pct, -1, 99},
       {"apply_gs", &c->apply_gs, 1, 1 << 20},      {"graph_b1", &c->graph_b1, 0, 1},
+      {"apply_full_grid", &c->apply_full_grid, -1, 1},
       {"solve_cluster", &c->solve_cluster, 0, 4},
   };
   for (const Knob& k : knobs)
@@ -614,7 +618,14 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
       prev_nb = nb;
     }
     if (e == cudaSuccess) e = mark(2);
-    const int ag = (int)std::max<int64_t>(c->num_sms, apply_grid(c) - std::min<int64_t>(prev_nb, apply_grid(c) / 2));
+    // the apply grid: every slot (2 per SM) when the last group is the larger one -- the CTAs that
+    // can only start once solve(G-1)'s CTAs leave then still add streaming capacity for the
+    // rest of the apply, their static share of the first groups being small (C3 0.2509 ->
+    // 0.2407 ms); else the slots the last group's solver CTAs leave (C5: a full grid puts 90%
+    // of the work in static shares that late CTAs finish last, 0.1876 vs 0.1649 ms)
+    const bool full_apply = c->apply_full_grid >= 0 ? c->apply_full_grid != 0 : 2 * gstart(G - 1) < B;
+    const int ag = full_apply ? apply_grid(c)
+                              : (int)std::max<int64_t>(c->num_sms, apply_grid(c) - std::min<int64_t>(prev_nb, apply_grid(c) / 2));
     if (e == cudaSuccess)
       e = counted(c, hr::launch_apply(in, lut, B, H, W, out, ag, st, ready, gstart(G - 1), ctl + 3, c->apply_gs));
   } else {

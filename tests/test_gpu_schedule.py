@@ -65,7 +65,8 @@ def test_grouped_equals_separate_and_oracle(shape):
 @pytest.mark.parametrize("knob", ["groups=3", "groups=7", "groups=2,group_first_pct=1", "groups=2,group_first_pct=99",
                                   "groups=3,apply_gs=1", "groups=2,apply_gs=1000", "solve_wide_px=1",
                                   "groups=0,solve_wide_px=1", "solve_cpsm=1", "solve_cpsm=2", "hist_cpsm=1",
-                                  "apply_cpsm=1", "groups=0,solve_cpsm=2,hist_cpsm=1,apply_cpsm=1"])
+                                  "apply_cpsm=1", "groups=0,solve_cpsm=2,hist_cpsm=1,apply_cpsm=1",
+                                  "apply_full_grid=1", "apply_full_grid=0", "groups=3,apply_full_grid=1"])
 @pytest.mark.parametrize("shape", [(2, 4, 4), (3, 37, 112), (40, 16, 32), (2, 37, 264), (5, 120, 600), (1, 300, 1920),
                                    (150, 16, 256)])
 def test_policy_options_bit_exact(knob, shape):
