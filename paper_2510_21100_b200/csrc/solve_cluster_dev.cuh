@@ -42,7 +42,8 @@ struct __align__(16) SmClusterExtra {
 
 // phase clocks (measurement builds, -DHR_SOLVE_PROFILE): rank 0 of block 0, thread 0;
 // g_solve_clk[700 + i]: 0 start, 1 supports, 2 keys, 3 runs, 4 iterations, 5 Eq. 20 + LUT;
-// [710 + j] per-phase sums over the iterations: E1, E2, E3, R, L (each to its closing barrier)
+// [720 + j] per-phase sums over the iterations: E1, E2, E3, R, L (each to its closing barrier);
+// 6-10: the tail's steps (tools/cluster_scan.py)
 #ifdef HR_SOLVE_PROFILE
 #define CMARK(i)                                                    \
   do {                                                              \
@@ -53,7 +54,7 @@ struct __align__(16) SmClusterExtra {
   do {                                                                                 \
     if (blockIdx.x == 0 && threadIdx.x == 0) {                                         \
       const long long t1_ = clock64();                                                 \
-      g_solve_clk[710 + (j)] += t1_ - cph_t0_;                                         \
+      g_solve_clk[720 + (j)] += t1_ - cph_t0_;                                         \
       cph_t0_ = t1_;                                                                   \
     }                                                                                  \
   } while (0)
@@ -102,7 +103,7 @@ __device__ int iterate_cluster(Sm& s, SmClusterExtra& x, cg::cluster_group& cl, 
   int t = 0;
 #ifdef HR_SOLVE_PROFILE
   if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int j = 0; j < 5; ++j) g_solve_clk[710 + j] = 0;
+    for (int j = 0; j < 5; ++j) g_solve_clk[720 + j] = 0;
 #endif
   CPH_T0();
   for (;;) {
@@ -398,6 +399,7 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
   int* rowOff = s.keyStart;
   uint8_t* kmin = reinterpret_cast<uint8_t*>(mask);
   __syncthreads();
+  CMARK(6);
   const int wr = tid < nRl ? (int)kc1[tid * nL + nL - 1] - (int)kc1[tid * nL] + 1 : 0;
   int Wtot;
   const int offr = block_scan_excl<T>(wr, &Wtot, wscr);
@@ -410,25 +412,9 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
   double* D = dS ? reinterpret_cast<double*>(arenaS + align16(El)) : reinterpret_cast<double*>(arenaG);
   for (int i = tid; i < Wtot; i += T) D[i] = 0.0;
   __syncthreads();
-  if (tid < nRl) {
-    const uint8_t* kr = kc1 + tid * nL;
-    const int k0 = kr[0];
-    double acc = 0.0;
-    int k = k0;
-    const double hra = s.hR[aB + tid];
-    for (int c = 0; c < nL; ++c) {
-      const int kn = kr[c];
-      if (kn != k) {
-        HR_CHECK(kn > k && offr + k - k0 < Wtot && k >= k0);
-        D[offr + k - k0] = hra * acc;
-        acc = 0.0;
-        k = kn;
-      }
-      acc += s.hL[c];
-    }
-    D[offr + k - k0] = hra * acc;
-  }
+  if (tid < nRl) row_runs(kc1 + tid * nL, nL, s.hL, s.hR[aB + tid], D, offr);  // local row tid
   __syncthreads();
+  CMARK(7);
   if (binT) {
     double e0 = 0.0;
     for (int a = 0; a < nRl; ++a) {
@@ -439,6 +425,7 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
     x.est[tid] = e0;
   }
   cluster_sync_all();
+  CMARK(8);
   if (out0) {
     double* Tt = s.rho;
     if (binT) {
@@ -448,13 +435,15 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
       Tt[tid] = e / N;
     }
     __syncthreads();
+    CMARK(9);
     if (args.target && binT) args.target[b * kLevels + tid] = Tt[tid];
     if (args.lut || args.status)
       cdf_lut<T>(s.hSi, Tt, s.hL1, s.wgt, s.hL2, wscr, args.lut ? args.lut + b * kLevels : nullptr,
                  args.status ? args.status + b : nullptr);
   }
-  CMARK(5);
+  CMARK(10);
   cluster_sync_all();  // rank 0's DSMEM reads are done before any CTA exits
+  CMARK(5);
 }
 
 }  // namespace

@@ -435,6 +435,39 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   SLOT_MARK(pslot + 6);
 }
 
+// One row's Eq. 20 run sums (keys kr[0..nL) non-decreasing): D[off + k - k0] = hra * (sum of
+// hL over the row's cells of key k), in column order.  Keys and hL are loaded 8 cells at a time
+// (all in flight together) before the sequential pass over them, so the walk does not wait for a
+// load per cell; the additions are the plain column-order ones.
+__device__ __forceinline__ void row_runs(const uint8_t* __restrict__ kr, int nL, const double* __restrict__ hL,
+                                         double hra, double* __restrict__ D, int off) {
+  const int k0 = kr[0];
+  double acc = 0.0;
+  int k = k0;
+  for (int c0 = 0; c0 < nL; c0 += 8) {
+    int kk[8];
+    double hv[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const bool in = c0 + m < nL;
+      kk[m] = in ? kr[c0 + m] : -1;
+      hv[m] = in ? hL[c0 + m] : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      if (kk[m] < 0) break;
+      HR_CHECK(kk[m] >= k);
+      if (kk[m] != k) {
+        D[off + k - k0] = hra * acc;
+        acc = 0.0;
+        k = kk[m];
+      }
+      acc += hv[m];
+    }
+  }
+  D[off + k - k0] = hra * acc;
+}
+
 // sum of h[lo..hi] (hi - lo < kPiece): all loads predicated and in flight at once, fixed tree
 __device__ __forceinline__ double piece_sum(const double* __restrict__ h, int lo, int hi) {
   const int n = hi - lo;
@@ -882,23 +915,7 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   HR_CHECK(dS || 8 * Wtot <= 12 * kMaxPieces);
   for (int i = tid; i < Wtot; i += T) D[i] = 0.0;
   __syncthreads();
-  if (tid < nR) {  // row a = tid: its runs in order
-    const uint8_t* kr = kc1 + tid * nL;
-    const int k0 = kr[0];
-    double acc = 0.0;
-    int k = k0;
-    for (int c = 0; c < nL; ++c) {
-      const int kn = kr[c];
-      HR_CHECK(kn >= k);
-      if (kn != k) {
-        D[offr + k - k0] = s.hR[tid] * acc;
-        acc = 0.0;
-        k = kn;
-      }
-      acc += s.hL[c];
-    }
-    D[offr + k - k0] = s.hR[tid] * acc;
-  }
+  if (tid < nR) row_runs(kc1 + tid * nL, nL, s.hL, s.hR[tid], D, offr);  // row a = tid
   __syncthreads();
   double* Tt = s.rho;  // dense target
   if (binT) {

@@ -25,9 +25,11 @@ for _ in range(3):
 torch.cuda.synchronize()
 full = (ctypes.c_longlong * 1024)()
 lib.hr_debug_solve_clocks_all(full)
-c = np.array(full[700:706], dtype=np.int64)
-ph = np.array(full[710:715], dtype=np.int64)
+c = np.array(full[700:711], dtype=np.int64)
+ph = np.array(full[720:725], dtype=np.int64)
 names = ["supports", "keys", "runs", "iterations", "eq20+lut"]
 print(f"{cfg}: cluster solve {(c[5] - c[0]) / GHZ / 1e3:.1f} us: " +
       " ".join(f"{n}={d}" for n, d in zip(names, np.diff(c).tolist())))
 print("  per-iteration sums E1/E2+sync/E3/R+sync/L+sync (cycles, all iterations):", ph.tolist())
+print("  tail: idx1 keys %d, row walks %d, bin sums + sync %d, combine %d, lut %d, final sync %d" % (
+    c[6] - c[4], c[7] - c[6], c[8] - c[7], c[9] - c[8], c[10] - c[9], c[5] - c[10]))
