@@ -56,31 +56,6 @@ __device__ __forceinline__ void load_strip(const uint8_t* __restrict__ p, uint32
       w[4 * i + 2] = a.z;
       w[4 * i + 3] = a.w;
     }
-  } else if constexpr (VEC == 9) {
-    // 8-B aligned rows whose 16-B alignment alternates (3 W % 16 == 8): 16-B aligned -> three
-    // 16-B loads; 8 mod 16 -> 8 + 16 + 16 + 8 B (4 loads instead of the six 8-B loads).  The
-    // branch is warp-uniform: every lane of a step reads a row of the same parity (RPG even)
-    static_assert(NWD == 12, "mixed-alignment loads are for 16-px strips");
-    if ((reinterpret_cast<uintptr_t>(p) & 8u) == 0) {
-      const uint4* q = reinterpret_cast<const uint4*>(p);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const uint4 a = __ldg(q + i);
-        w[4 * i] = a.x;
-        w[4 * i + 1] = a.y;
-        w[4 * i + 2] = a.z;
-        w[4 * i + 3] = a.w;
-      }
-    } else {
-      const uint2 a = __ldg(reinterpret_cast<const uint2*>(p));
-      const uint4 b = __ldg(reinterpret_cast<const uint4*>(p + 8));
-      const uint4 c = __ldg(reinterpret_cast<const uint4*>(p + 24));
-      const uint2 d = __ldg(reinterpret_cast<const uint2*>(p + 40));
-      w[0] = a.x, w[1] = a.y;
-      w[2] = b.x, w[3] = b.y, w[4] = b.z, w[5] = b.w;
-      w[6] = c.x, w[7] = c.y, w[8] = c.z, w[9] = c.w;
-      w[10] = d.x, w[11] = d.y;
-    }
   } else if constexpr (VEC == 8) {
     const uint2* q = reinterpret_cast<const uint2*>(p);
 #pragma unroll
@@ -210,18 +185,7 @@ __device__ __forceinline__ void walk_strip(const uint8_t* __restrict__ p, size_t
   for (int q = 0; q < G; ++q) Vp[q] = Dp[q] = 0u;
   auto need = [&](int it) { return it < nr || (it == nr && halo); };  // row ya+it is read
   auto load_row = [&](const uint8_t* pr, uint32_t (&wr)[3 * G], uint32_t& nbr) {
-    if constexpr (G == 4) {
-      load_strip<16, VEC>(pr, wr);
-    } else {  // half strip (8 px, 24 B, 8-B aligned)
-      static_assert(G == 2, "");
-      const uint2* q = reinterpret_cast<const uint2*>(pr);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const uint2 a = __ldg(q + i);
-        wr[2 * i] = a.x;
-        wr[2 * i + 1] = a.y;
-      }
-    }
+    load_strip<4 * G, VEC>(pr, wr);
     nbr = rowEnd ? 0u : load_nb<VEC>(pr + 12 * G);
   };
   // step it: row ya+it -> value channel, H_C(S) counts, dx; gradient of row ya+it-1
@@ -275,10 +239,6 @@ __device__ __forceinline__ void walk_strip(const uint8_t* __restrict__ p, size_t
 // Histogram rows [y0, y1) of one H x W image `img` into the (zeroed) lane-private counters
 // `sm`, then flush them with integer atomics into hist_s_b[256] / hist_graw_b[512].  All NT
 // threads call it; it ends with a barrier (the counters are then free for reuse, not zero).
-// W % 16 == 8 with 8-B aligned rows (VEC 8/9): the last 8 columns of each row are "half strips"
-// walked by a warp of their own (from the first multiple of 32 past the full-strip threads, up
-// to 32 walkers with row bands of their own, so the warp runs with all lanes busy) so neither
-// kind of warp diverges; fewer full-strip row groups when that leaves < 16 spare threads.
 template <int SW, int VEC, int NT>
 __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, int H, int W, int y0, int y1,
                                              uint32_t* sm, uint32_t* __restrict__ hist_s_b,
@@ -292,16 +252,9 @@ __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, in
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
 
   const int SPf = W / SW;   // full strips per row
-  int xt = SPf * SW;        // first column of the scalar tail
+  const int xt = SPf * SW;  // first column of the scalar tail
   const int SPt = SPf < NT ? SPf : NT;
-  int NG = SPf == 0 ? 0 : (SPf < NT ? NT / SPf : 1);  // row groups
-  const bool half = SW == 16 && (VEC == 8 || VEC == 9) && W - xt == 8 && SPf > 0 && SPf < NT;
-  if (half)
-    while (NG > 1 && ((NG * SPf + 31) & ~31) + 16 > NT) --NG;
-  const int TH = ((NG * SPf + 31) & ~31);  // first half-strip thread
-  const int HT = min(32, NT - TH);         // half-strip walkers: one warp, own row bands
-  const bool halfOk = half && HT >= 16;
-  if (halfOk) xt = W;  // no scalar tail
+  const int NG = SPf == 0 ? 0 : (SPf < NT ? NT / SPf : 1);  // row groups
   const int ntile = (SPf + NT - 1) / NT;
   const int grp = SPt ? tid / SPt : 0;
   const int sl = SPt ? tid - grp * SPt : 0;
@@ -313,32 +266,20 @@ __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, in
   // y+1 is loaded before row y is processed, so two rows of loads are in flight per thread.
   if (NG > 0) {
     const int nrows = y1 - y0;
-    int RPG = (nrows + NG - 1) / NG;
-    if constexpr (VEC == 9) RPG += RPG & 1;  // even: the rows of one step share their parity
-    if (halfOk && tid >= TH) {  // half-strip walkers (a warp of its own, or idle)
-      const int g = tid - TH;
-      const int RPH = (nrows + HT - 1) / HT;  // rows per half-strip band (bands of their own)
-      const int ya = y0 + g * RPH;
-      const int yb = min(y1, ya + RPH);
-      const bool act = g < HT && ya < yb;
-      const int nr = act ? yb - ya : 0;
-      const uint8_t* p = img + (size_t)(act ? ya : 0) * rowBytes + (size_t)(SPf * SW) * 3;
-      walk_strip<2, VEC>(p, rowBytes, RPH, nr, act && yb < H, true, sb, ghi, Lv, Lg);
-    } else {
-      for (int tile = 0; tile < ntile; ++tile) {
-        const int s = tile * NT + sl;
-        const bool act = (grp < NG) && (s < SPf) && (y0 + grp * RPG < min(y1, y0 + grp * RPG + RPG));
-        const int ya = y0 + grp * RPG;
-        const int yb = min(y1, ya + RPG);
-        const int nr = act ? yb - ya : 0;  // rows of this thread's band
-        const bool halo = act && yb < H;   // row yb exists: the gradient of row yb-1 needs it
-        const int x0 = act ? s * SW : 0;
-        const bool rowEnd = (s == SPf - 1) && (xt == W) && !halfOk;  // last pixel of this strip is x = W-1
-        const uint8_t* p = img + (size_t)(act ? ya : 0) * rowBytes + (size_t)x0 * 3;
-        // the first strip of each row group prefetches the group's whole rows into L2
-        const uintptr_t img_end = (reinterpret_cast<uintptr_t>(img) + (size_t)H * rowBytes) & ~(uintptr_t)15;
-        walk_strip<G, VEC>(p, rowBytes, RPG, nr, halo, rowEnd, sb, ghi, Lv, Lg, act && s == 0 && HR_HIST_PF > 0, img_end);
-      }
+    const int RPG = (nrows + NG - 1) / NG;
+    for (int tile = 0; tile < ntile; ++tile) {
+      const int s = tile * NT + sl;
+      const bool act = (grp < NG) && (s < SPf) && (y0 + grp * RPG < min(y1, y0 + grp * RPG + RPG));
+      const int ya = y0 + grp * RPG;
+      const int yb = min(y1, ya + RPG);
+      const int nr = act ? yb - ya : 0;  // rows of this thread's band
+      const bool halo = act && yb < H;   // row yb exists: the gradient of row yb-1 needs it
+      const int x0 = act ? s * SW : 0;
+      const bool rowEnd = (s == SPf - 1) && (xt == W);  // last pixel of this strip is x = W-1
+      const uint8_t* p = img + (size_t)(act ? ya : 0) * rowBytes + (size_t)x0 * 3;
+      // the first strip of each row group prefetches the group's whole rows into L2
+      const uintptr_t img_end = (reinterpret_cast<uintptr_t>(img) + (size_t)H * rowBytes) & ~(uintptr_t)15;
+      walk_strip<G, VEC>(p, rowBytes, RPG, nr, halo, rowEnd, sb, ghi, Lv, Lg, act && s == 0 && HR_HIST_PF > 0, img_end);
     }
   }
 

@@ -85,9 +85,8 @@ int hist_grid_clamped(int64_t B, int32_t H, int grid) {
 
 cudaError_t init_attrs_hist() {
   cudaError_t e = cudaSuccess;
-  for (auto k : {k_hist<16, 16, kHistThreads>, k_hist<16, 9, kHistThreads>, k_hist<8, 8, kHistThreads>,
-                 k_hist<16, 1, kHistThreads>, k_hist<16, 16, 1024>, k_hist<16, 9, 1024>, k_hist<8, 8, 1024>,
-                 k_hist<16, 1, 1024>})
+  for (auto k : {k_hist<16, 16, kHistThreads>, k_hist<8, 8, kHistThreads>, k_hist<16, 1, kHistThreads>,
+                 k_hist<16, 16, 1024>, k_hist<8, 8, 1024>, k_hist<16, 1, 1024>})
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistDevSmem);
   return e;
 }
@@ -97,10 +96,9 @@ cudaError_t launch_hist(const uint8_t* rgb, int64_t B, int32_t H, int32_t W, uin
   const uintptr_t a = reinterpret_cast<uintptr_t>(rgb);
   grid = hist_grid_clamped(B, H, grid);
   if (a % 16 == 0 && W % 16 == 0) return launch_v<16, 16>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait, nt);
-  // 8-B aligned rows, W % 16 == 8: 16-px strips with mixed 16-B / 8-B loads by row parity and
-  // half-strip walkers for the last 8 columns; other W % 8 == 0: 8-px strips
-  if (a % 8 == 0 && W % 8 == 0 && W >= 16)
-    return launch_v<16, 9>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait, nt);
+  // 8-B aligned rows (W % 16 == 8, e.g. C5's 600-px rows: a 1,800-B stride alternates between 0
+  // and 8 mod 16): 8-px strips of three 8-B loads (C5 58 vs 61 us with the round-1 16-px strips
+  // of mixed 16/8-B loads plus half-strip walkers, which needed 20 B of spills)
   if (a % 8 == 0 && W % 8 == 0) return launch_v<8, 8>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait, nt);
   return launch_v<16, 1>(rgb, B, H, W, hist_s, hist_graw, grid, done, st, nowait, nt);
 }

@@ -2,7 +2,7 @@
 
 The execution policy (hr_set_policy) is performance-only: every output (pixels, hist_s, LUT,
 iteration counts) must be bit-identical whatever the knobs, and equal to the oracle.  Shapes
-cover the histogram kernel's template paths (W % 16 == 0, W % 16 == 8 with half strips, W % 8,
+cover the histogram kernel's template paths (W % 16 == 0: 16-px strips, W % 8 == 0: 8-px strips,
 byte loads), H*W % 16 != 0 (the scalar apply), one-row images, batches larger than the grid,
 and degenerate images next to normal ones.
 """
