@@ -56,11 +56,15 @@ constexpr int kPiece = HR_KPIECE;
 static_assert(kPiece == 8 || kPiece == 16, "piece length");
 constexpr int kMaxRuns = 32896;                        // sum_{i<256} (i + 1): runs of any image
 constexpr int kMaxPieces = kMaxRuns + 65536 / kPiece;  // P <= RR + E / kPiece
+constexpr int kChunk = 8;                              // cells per chunk (k_solve: bin-ordered chunks)
+constexpr int kMaxChunks = 65536 / kChunk + 256;       // each bin's last chunk may be partial
 constexpr int kMaskBytes = kLevels * 8 * 4;            // per-bin row bitmask (8 words per bin)
 constexpr int kArenaSmem = 80 * 1024;  // default shared arena: keys (E bytes) + run arena + mask tail
 constexpr int kKeysGlobal = 65536;      // keys of images whose keys do not fit the shared arena
-constexpr int kArenaGlobal = 12 * kMaxPieces + 256 + kKeysGlobal;  // per-image global arena
-static_assert(8 * kMaxPieces >= 8 * kMaxRuns, "build scratch must fit under pVal");
+// per-image global arena: descriptors + max(values, build scratch) of either form, then keys
+constexpr int kArenaRun = 4 * kChunk * kMaxChunks + 8 * kMaxRuns + 256;
+constexpr int kArenaGlobal = kArenaRun + kKeysGlobal;
+static_assert(kArenaRun >= 12 * kMaxPieces + 256, "the piece form fits too");
 
 // Phase clock marks (measurement builds only: -DHR_SOLVE_PROFILE; block kProfBlock, thread 0).
 #ifdef HR_SOLVE_PROFILE
@@ -94,7 +98,8 @@ enum { R_SL2 = 0, R_SR1, R_SR2, R_SL1, R_DR, R_DL, R_QL1, R_OBJ, kSlots };
 
 struct __align__(16) Sm {
   double hR[kLevels], hL[kLevels];    // renormalised state (index a over sR, c over sL)
-  double hR1[kLevels], hL1[kLevels];  // raw updates (Eq. 13 / Eq. 12 outputs)
+  double hR1[kLevels], hL1[kLevels + 2];  // raw updates (Eq. 13 / Eq. 12 outputs); hL1[256] = 0: the
+                                          // factor of a chunk's unused cell slots
   double hSc[kLevels], hGc[kLevels];  // priors at the support entries
   double hL2[kLevels];                // hL_c^2
   double wgt[kLevels];                // per-row weight of the L-walk
@@ -104,6 +109,7 @@ struct __align__(16) Sm {
   double red[kSlots][kMaxSW];
   uint32_t hSi[kLevels], hGi[kLevels];
   int keyStart[kLevels + 1];  // piece offsets per bin (bin order)
+  int pStart[kLevels], cBase[kLevels];  // run_build (chunks): a bin's first chunk / first cell
   uint8_t listR[kLevels], listL[kLevels];
   uint8_t binList[kLevels];   // the bins holding pieces, ascending (E2: lanes per bin)
   int nBins;
@@ -320,10 +326,18 @@ struct RunArena {
 // its bin-ordered slot = (runs of smaller bins) + rank of its row among the bin's rows.  A
 // scan of the per-slot piece counts places every piece in bin order.  Placement: after the
 // keys in shared memory when it fits (mask tail excluded), else arenaG.
+// chunks (k_solve): instead of pieces of a run, the CELLS are laid out in bin order (bin, then
+// row, then column) and cut into chunks of kChunk cells that never straddle a bin (a bin's last
+// chunk is padded with slots whose factor is hL1[256] = 0): chunk p = pDesc[8p .. 8p + 8), a cell
+// = (byte offset of hR1_a) | (byte offset of hL1_c) << 16; s.keyStart = chunk offsets per bin.
+// The E1 phase is then one chunk (8 independent products, a fixed tree) per thread with ~E / 8 +
+// (bins) chunks in all -- row-run pieces are mostly 1-2 cells long when the rows are sparse (a
+// MAXNORM gradient support), so there were ~5 per thread.
 template <int T>
 __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* mask, unsigned char* arenaS,
                           int arenaBytes, bool keysInSmem, unsigned char* arenaG, RunArena& A, int* wscr,
-                          int pslot = 0) {
+                          bool chunks = false, int pslot = 0) {
+  constexpr int plen = kPiece;
   const int tid = threadIdx.x;
   SLOT_MARK(pslot + 0);
   const int E = nR * nL;
@@ -343,13 +357,15 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   int RR;
   int r = block_scan_excl<T>(cnt, &RR, wscr);
   SLOT_MARK(pslot + 1);
-  const int Pmax = RR + E / kPiece;
+  const int Pmax = chunks ? E / kChunk + kLevels : RR + E / plen;
   HR_CHECK(RR >= nR && RR <= E && RR <= kMaxRuns);
   const int keysS = keysInSmem ? align16(E) : 0;
-  const bool sm = keysS + align16(4 * Pmax) + 8 * Pmax <= arenaBytes - kMaskBytes;
+  const int descB = align16(chunks ? 4 * kChunk * Pmax : 4 * Pmax);
+  const int valB = 8 * (Pmax > RR ? Pmax : RR);  // piece values; the build scratch before that
+  const bool sm = keysS + descB + valB <= arenaBytes - kMaskBytes;
   unsigned char* base = sm ? arenaS + keysS : arenaG;
   A.pDesc = reinterpret_cast<uint32_t*>(base);
-  A.pVal = reinterpret_cast<double*>(base + align16(4 * Pmax));
+  A.pVal = reinterpret_cast<double*>(base + descB);
   A.RR = RR;
   uint32_t* runDesc = reinterpret_cast<uint32_t*>(A.pVal);  // build scratch under pVal
   uint32_t* slotN = runDesc + RR;                           // bin order: pieces, then offsets
@@ -395,7 +411,7 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
     HR_CHECK(lo <= hi && hi < nL && a < nR);
     HR_CHECK(s.keyStart[k] + mask_rank(mask + k * 8, a) < RR);
-    slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)] = (uint32_t)((hi - lo) / kPiece + 1);
+    slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)] = (uint32_t)(chunks ? hi - lo + 1 : (hi - lo) / plen + 1);
   }
   __syncthreads();
   SLOT_MARK(pslot + 4);
@@ -409,20 +425,50 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     off += n;
   }
   A.P = P;
-  HR_CHECK(P >= RR && P <= Pmax && RK == RR);
+  HR_CHECK(RK == RR && (chunks ? P == E : P >= RR && P <= Pmax));
   __syncthreads();
   SLOT_MARK(pslot + 5);
-  for (int q = r0; q < r1; ++q) {  // pieces of each run at its bin-order offset
-    const uint32_t d = runDesc[q];
-    const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
-    int p = (int)slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)];
-    for (int l = lo; l <= hi; l += kPiece, ++p)
-      A.pDesc[p] = (uint32_t)l | ((uint32_t)min(l + kPiece - 1, hi) << 8) | ((uint32_t)a << 16);
-    HR_CHECK(p <= P);
+  if (chunks) {
+    // cells per bin -> chunks per bin -> chunk offsets (a scan over the bins)
+    int nc = 0, cs = 0;
+    if (tid < kLevels) {
+      cs = kfirst < RK ? (int)slotN[kfirst] : P;
+      const int kn = kfirst + kcount;  // the next bin's first run slot
+      nc = ((kn < RK ? (int)slotN[kn] : P) - cs + kChunk - 1) / kChunk;
+    }
+    int PC;
+    const int ps = block_scan_excl<T>(nc, &PC, wscr);
+    HR_CHECK(PC <= Pmax);
+    if (tid < kLevels) {
+      s.pStart[tid] = ps;
+      s.cBase[tid] = cs;
+    }
+    for (int i = tid; i < kChunk * PC; i += T) A.pDesc[i] = (uint32_t)(8 * kLevels) << 16;  // unused: hR1_0 * hL1[256]
+    __syncthreads();
+    for (int q = r0; q < r1; ++q) {  // the cells of each run at its bin-order position
+      const uint32_t d = runDesc[q];
+      const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
+      int p = kChunk * s.pStart[k] + (int)slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)] - s.cBase[k];
+      HR_CHECK(p >= 0 && p + hi - lo < kChunk * PC);
+      for (int l = lo; l <= hi; ++l, ++p) A.pDesc[p] = (uint32_t)(8 * a) | ((uint32_t)(8 * l) << 16);
+    }
+    __syncthreads();
+    if (tid < kLevels) s.keyStart[tid] = s.pStart[tid];  // run slots -> chunk offsets
+    if (tid == 0) s.keyStart[kLevels] = PC;
+    A.P = PC;
+  } else {
+    for (int q = r0; q < r1; ++q) {  // pieces of each run at its bin-order offset
+      const uint32_t d = runDesc[q];
+      const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
+      int p = (int)slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)];
+      for (int l = lo; l <= hi; l += plen, ++p)
+        A.pDesc[p] = (uint32_t)l | ((uint32_t)min(l + plen - 1, hi) << 8) | ((uint32_t)a << 16);
+      HR_CHECK(p <= P);
+    }
+    __syncthreads();
+    if (tid < kLevels) s.keyStart[tid] = kfirst < RK ? (int)slotN[kfirst] : P;  // run slots -> piece offsets
+    if (tid == 0) s.keyStart[kLevels] = P;
   }
-  __syncthreads();
-  if (tid < kLevels) s.keyStart[tid] = kfirst < RK ? (int)slotN[kfirst] : P;  // run slots -> piece offsets
-  if (tid == 0) s.keyStart[kLevels] = P;
   __syncthreads();
   {  // the bins holding pieces, ascending
     const bool has = tid < kLevels && s.keyStart[tid] < s.keyStart[tid + 1];
@@ -546,18 +592,20 @@ __device__ double objective(Sm& s, const hr_params& P, int nR, int nL, double N,
   return F;
 }
 
-// Algorithm 1 iterations over the run arena A.  Returns t.
+// Algorithm 1 iterations over the chunk arena A (run_build with chunks: the cells in bin order,
+// 8 per chunk).  Returns t; s.hR, s.hL then hold the renormalised final iterates (barrier done).
+// The iterates stay RAW (s.hR1, s.hL1, the outputs of Eqs. 13 / 12); the factors of Eqs. 15, 14,
+// cR = N / sum hR1 and cL = N / sum hL1, are applied as scalars where a renormalised value
+// enters, so no phase waits for a renormalisation pass.
 // Four phases per update, each closed by a barrier:
-//   E1  renormalise the raw iterates of the previous update (Eqs. 15, 14) and, one thread per
-//       piece, hR_a * sum(hL) over the piece (Eqs. 6, 8)
-//   E2  one thread per bin: EstRaw_k over the bin's runs in row order, rho_k (Eq. 11 folded)
+//   E1  one chunk per thread: the sum of its 8 cell products hR1_a hL1_c (Eqs. 6, 8)
+//   E2  TPB lanes per occupied bin: EstRaw_k = cR cL sum of the bin's chunks; rho_k (Eq. 11 folded)
 //   R   TPR threads per row: A_a over the row's cells (cached keys kc), Eq. 13
 //   L   TPC threads per column: B_c over the rows, Eq. 12 with the frozen K
+// Before the call: s.hR1 = s.hR = hG, s.hL1 = s.hL = hS (support entries), s.hL2 = hS^2, slot
+// R_QL1 = per-warp partials of sum hS^2 (barrier done).
 // kTrace: the Eq. 10 objective trace (hr_solve_trace) is compiled into a separate instance, so
-// the product loop stays small (its body must stay resident in the instruction caches: one CTA
-// per image repeats it T times)
-// kForm: P.update_form as a compile-time constant (each instance carries one form's loops only:
-// a smaller loop body for the instruction caches)
+// the product loop stays small.  kForm: P.update_form as a compile-time constant.
 template <int T, bool kTrace, int kForm>
 __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL, double N, const uint8_t* kc,
                                        const RunArena& A, double* trace = nullptr, int trace_cap = 0) {
@@ -572,8 +620,18 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
   const int TPB = 1 << lgB;
   constexpr int form = kForm;
   const double invN = 1.0 / N, invN2 = invN * invN;
+  // this thread's share of the E2 phase: lane qb of the TPB lanes of bin kb (fixed for all t)
+  const int jb = tid >> lgB, qb = tid & (TPB - 1);
+  int kb = 0, pbeg = 0, pend = 0;
+  if (jb < nBins) {
+    kb = s.binList[jb];
+    pbeg = s.keyStart[kb] + qb;
+    pend = s.keyStart[kb + 1];
+  }
+  const double hSk = s.hSd[kb];
+  const bool diffs = P.use_epsilon || kTrace;  // the renormalised iterates are needed every update
   double SR1 = N, SL1 = N;  // sums of the raw iterates (initially exactly N)
-  double QL1 = 0.0;          // sum of the raw hL iterate squared (from the L phase, t > 0)
+  double QL1 = slot_sum<T>(s, R_QL1);
   int t = 0;
 #ifdef HR_SOLVE_PROFILE
   long long pacc[16] = {0}, pt0 = clock64(), pt1;
@@ -582,86 +640,76 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
 #define PHASE(i) do { } while (0)
 #endif
   for (;;) {
-    // ======== E1: renormalise (Eqs. 15, 14); piece sums (Eqs. 6, 8) ========
-    // sum hL^2 of the renormalised hL = cL^2 * QL1 (reduced in the L phase); the block
-    // reduction here is only needed for t = 0 and for the stop rule
-    const double cL = N * rcp_fast(SL1);
+    if (t > 0 && !P.use_epsilon && t >= P.max_iter) break;
+    // Eqs. 15, 14 as scalars: hR = cR hR1, hL = cL hL1
+    const double cR = N * rcp_fast(SR1), cL = N * rcp_fast(SL1);
+    // ======== E1: one chunk per thread: 8 cell products (Eqs. 6, 8) in flight, a fixed tree ========
     {
-      const double cR = N * rcp_fast(SR1), cRL = cR * cL;
-      double dr = 0.0, dl = 0.0, q = 0.0;
-      if (tid < nR) {
-        const double n = cR * s.hR1[tid];
-        dr = (n - s.hR[tid]) * (n - s.hR[tid]);
-        s.hR[tid] = n;
-      }
-      if (tid < nL) {
-        const double n = cL * s.hL1[tid];
-        dl = (n - s.hL[tid]) * (n - s.hL[tid]);
-        s.hL[tid] = n;
-        s.hL2[tid] = n * n;
-        q = n * n;
-      }
-      PHASE(7);
-      {  // piece sums hR_a * sum(hL over the piece); two pieces per step so that their loads
-         // are in flight together (restrict: the stores to pVal cannot alias the loads)
-        const uint32_t* __restrict__ pd = A.pDesc;
-        double* __restrict__ pv = A.pVal;
-        const double* __restrict__ hl1 = s.hL1;
-        const double* __restrict__ hr1 = s.hR1;
-        int p = tid;
-        for (; p + T < A.P; p += 2 * T) {
-          const uint32_t d0 = pd[p], d1 = pd[p + T];
-          const double v0 = hr1[d0 >> 16] * piece_sum(hl1, d0 & 255, (d0 >> 8) & 255) * cRL;
-          const double v1 = hr1[d1 >> 16] * piece_sum(hl1, d1 & 255, (d1 >> 8) & 255) * cRL;
-          pv[p] = v0;
-          pv[p + T] = v1;
-        }
-        if (p < A.P) {
-          const uint32_t d = pd[p];
-          pv[p] = hr1[d >> 16] * piece_sum(hl1, d & 255, (d >> 8) & 255) * cRL;
-        }
+      const uint4* __restrict__ cd = reinterpret_cast<const uint4*>(A.pDesc);
+      double* __restrict__ pv = A.pVal;
+      const unsigned char* __restrict__ hrb = reinterpret_cast<const unsigned char*>(s.hR1);
+      const unsigned char* __restrict__ hlb = reinterpret_cast<const unsigned char*>(s.hL1);
+      for (int p = tid; p < A.P; p += T) {
+        const uint4 q0 = cd[2 * p], q1 = cd[2 * p + 1];
+        const uint32_t d[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        double x[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+          x[m] = *reinterpret_cast<const double*>(hrb + (d[m] & 0xFFFFu)) *
+                 *reinterpret_cast<const double*>(hlb + (d[m] >> 16));
+#pragma unroll
+        for (int w = 1; w < 8; w <<= 1)
+#pragma unroll
+          for (int m = 0; m + w < 8; m += 2 * w) x[m] += x[m + w];
+        pv[p] = x[0];
       }
       PHASE(8);
-      if (t == 0 || P.use_epsilon) slot_put3(s, R_DR, dr, R_DL, dl, R_SL2, q);
+      if (diffs && t > 0) {  // stop rule (R11): the renormalised iterates of update t against t-1
+        double dr = 0.0, dl = 0.0;
+        if (tid < nR) {
+          const double n = cR * s.hR1[tid];
+          dr = (n - s.hR[tid]) * (n - s.hR[tid]);
+          s.hR[tid] = n;
+        }
+        if (tid < nL) {
+          const double n = cL * s.hL1[tid];
+          dl = (n - s.hL[tid]) * (n - s.hL[tid]);
+          s.hL[tid] = n;
+        }
+        if (P.use_epsilon) slot_put3(s, R_DR, dr, R_DL, dl, -1, 0.0);
+      }
     }
     PHASE(9);
     __syncthreads();
     PHASE(0);
-    if (t > 0) {  // stop rule (R11) on the renormalised iterates of update t
+    if (P.use_epsilon && t > 0) {
       const double eps = P.epsilon * N * N;
-      const bool conv = P.use_epsilon && slot_sum<T>(s, R_DR) <= eps && slot_sum<T>(s, R_DL) <= eps;
-      if (conv || t >= P.max_iter) break;
+      if ((slot_sum<T>(s, R_DR) <= eps && slot_sum<T>(s, R_DL) <= eps) || t >= P.max_iter) break;
     }
-    PHASE(14);
-    // ======== E2: EstRaw_k over the bin's pieces (bin order); rho_k (Eq. 11) ========
+    // ======== E2: EstRaw_k = cR cL (sum of the bin's cell products, bin order); rho_k (Eq. 11) ========
     // TPB lanes per occupied bin (the largest power of two <= 32 with every bin covered), each
-    // summing every TPB-th piece, then a fixed shuffle tree over the TPB lanes
+    // summing every TPB-th product, then a fixed shuffle tree over the TPB lanes
     {
-      const int j = tid >> lgB, q = tid & (TPB - 1);
+      const double* __restrict__ pv = A.pVal;
       double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
-      int k = 0;
-      if (j < nBins) {
-        k = s.binList[j];
-        const int j1 = s.keyStart[k + 1];
-        const double* __restrict__ pv = A.pVal;
-        int i = s.keyStart[k] + q;
-        for (; i + 3 * TPB < j1; i += 4 * TPB) {
-          e0 += pv[i];
-          e1 += pv[i + TPB];
-          e2 += pv[i + 2 * TPB];
-          e3 += pv[i + 3 * TPB];
-        }
-        if (i < j1) e0 += pv[i];
-        if (i + TPB < j1) e1 += pv[i + TPB];
-        if (i + 2 * TPB < j1) e2 += pv[i + 2 * TPB];
+      int i = pbeg;
+      for (; i + 3 * TPB < pend; i += 4 * TPB) {
+        e0 += pv[i];
+        e1 += pv[i + TPB];
+        e2 += pv[i + 2 * TPB];
+        e3 += pv[i + 3 * TPB];
       }
+      if (i < pend) e0 += pv[i];
+      if (i + TPB < pend) e1 += pv[i + TPB];
+      if (i + 2 * TPB < pend) e2 += pv[i + 2 * TPB];
       double e = (e0 + e1) + (e2 + e3);
       for (int d = 1; d < TPB; d <<= 1) e += __shfl_xor_sync(0xffffffffu, e, d);
-      if (j < nBins && q == 0)  // EstRaw_k (Eqs. 6, 8)
-        s.rho[k] = form == 0 ? (e > 0.0 ? s.hSd[k] * rcp_fast(e) : 0.0) : s.hSd[k] * e;
+      PHASE(15);
+      if (jb < nBins && qb == 0) {
+        const double er = e * (cR * cL);  // EstRaw_k of the renormalised iterates
+        s.rho[kb] = form == 0 ? (er > 0.0 ? hSk * rcp_fast(er) : 0.0) : hSk * er;
+      }
     }
-    PHASE(15);
-    const double invDenR = rcp_fast((t == 0 ? slot_sum<T>(s, R_SL2) : cL * cL * QL1) * invN2 + P.beta);
     PHASE(10);
     __syncthreads();
     PHASE(1);
@@ -670,41 +718,45 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       if (tid == 0 && 3 * t < trace_cap) trace[3 * t] = F;
     }
     // ======== R: Eq. 13, TPR threads per row walking every TPR-th cell, fixed-order reduce ========
+    const double cL2 = cL * cL;
     {
+      const double invDenR = rcp_fast(cL2 * QL1 * invN2 + P.beta);
       double A0 = 0.0, A1 = 0.0;
       const int a = tid >> lgR, p = tid & (TPR - 1);
       if (a < nR) {
-        const uint8_t* kr = kc + a * nL;
+        const uint8_t* __restrict__ kr = kc + a * nL;
+        const double* __restrict__ q2 = s.hL2;
+        const double* __restrict__ rho = s.rho;
         int c = p;
-        if (form == 0) {  // four cells per step: keys, then rho and hL^2, all in flight
+        if (form == 0) {  // four cells per step: keys, then rho and hL1^2, all in flight
           double A2 = 0.0, A3 = 0.0;
           for (; c + 3 * TPR < nL; c += 4 * TPR) {
             const int k0 = kr[c], k1 = kr[c + TPR], k2 = kr[c + 2 * TPR], k3 = kr[c + 3 * TPR];
-            A0 = fma(s.hL2[c], s.rho[k0], A0);
-            A1 = fma(s.hL2[c + TPR], s.rho[k1], A1);
-            A2 = fma(s.hL2[c + 2 * TPR], s.rho[k2], A2);
-            A3 = fma(s.hL2[c + 3 * TPR], s.rho[k3], A3);
+            A0 = fma(q2[c], rho[k0], A0);
+            A1 = fma(q2[c + TPR], rho[k1], A1);
+            A2 = fma(q2[c + 2 * TPR], rho[k2], A2);
+            A3 = fma(q2[c + 3 * TPR], rho[k3], A3);
           }
-          if (c < nL) A0 = fma(s.hL2[c], s.rho[kr[c]], A0);
-          if (c + TPR < nL) A1 = fma(s.hL2[c + TPR], s.rho[kr[c + TPR]], A1);
-          if (c + 2 * TPR < nL) A2 = fma(s.hL2[c + 2 * TPR], s.rho[kr[c + 2 * TPR]], A2);
+          if (c < nL) A0 = fma(q2[c], rho[kr[c]], A0);
+          if (c + TPR < nL) A1 = fma(q2[c + TPR], rho[kr[c + TPR]], A1);
+          if (c + 2 * TPR < nL) A2 = fma(q2[c + 2 * TPR], rho[kr[c + 2 * TPR]], A2);
           A0 += A2;
           A1 += A3;
         } else {
           for (; c + TPR < nL; c += 2 * TPR) {
-            A0 += s.rho[kr[c]];
-            A1 += s.rho[kr[c + TPR]];
+            A0 += rho[kr[c]];
+            A1 += rho[kr[c + TPR]];
           }
-          if (c < nL) A0 += s.rho[kr[c]];
+          if (c < nL) A0 += rho[kr[c]];
         }
       }
       PHASE(4);
-      double A = A0 + A1;
-      for (int d = TPR >> 1; d >= 1; d >>= 1) A += __shfl_xor_sync(0xffffffffu, A, d);
+      double Av = A0 + A1;
+      for (int d = TPR >> 1; d >= 1; d >>= 1) Av += __shfl_xor_sync(0xffffffffu, Av, d);
       double v = 0.0;
       if (a < nR && p == 0) {
-        const double hr = s.hR[a];
-        const double num = form == 0 ? hr * A * invN : A * rcp_fast(N * hr);
+        const double hr = cR * s.hR1[a];  // renormalised hR_a of update t
+        const double num = form == 0 ? hr * (cL2 * Av) * invN : Av * rcp_fast(N * hr);
         v = (num + P.beta * s.hGc[a]) * invDenR;
         v = v > 0.0 ? v : 0.0;
         s.hR1[a] = v;
@@ -726,19 +778,21 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       double B0 = 0.0, B1 = 0.0;
       const int c = tid >> lgL, p = tid & (TPC - 1);
       if (c < nL) {
-        const uint8_t* kq = kc + c;
+        const uint8_t* __restrict__ kq = kc + c;
+        const double* __restrict__ wg = s.wgt;
+        const double* __restrict__ rho = s.rho;
         int a = p;
         double B2 = 0.0, B3 = 0.0;
         for (; a + 3 * TPC < nR; a += 4 * TPC) {  // four cells per step, keys first
           const int k0 = kq[a * nL], k1 = kq[(a + TPC) * nL], k2 = kq[(a + 2 * TPC) * nL], k3 = kq[(a + 3 * TPC) * nL];
-          B0 = fma(s.wgt[a], s.rho[k0], B0);
-          B1 = fma(s.wgt[a + TPC], s.rho[k1], B1);
-          B2 = fma(s.wgt[a + 2 * TPC], s.rho[k2], B2);
-          B3 = fma(s.wgt[a + 3 * TPC], s.rho[k3], B3);
+          B0 = fma(wg[a], rho[k0], B0);
+          B1 = fma(wg[a + TPC], rho[k1], B1);
+          B2 = fma(wg[a + 2 * TPC], rho[k2], B2);
+          B3 = fma(wg[a + 3 * TPC], rho[k3], B3);
         }
-        if (a < nR) B0 = fma(s.wgt[a], s.rho[kq[a * nL]], B0);
-        if (a + TPC < nR) B1 = fma(s.wgt[a + TPC], s.rho[kq[(a + TPC) * nL]], B1);
-        if (a + 2 * TPC < nR) B2 = fma(s.wgt[a + 2 * TPC], s.rho[kq[(a + 2 * TPC) * nL]], B2);
+        if (a < nR) B0 = fma(wg[a], rho[kq[a * nL]], B0);
+        if (a + TPC < nR) B1 = fma(wg[a + TPC], rho[kq[(a + TPC) * nL]], B1);
+        if (a + 2 * TPC < nR) B2 = fma(wg[a + 2 * TPC], rho[kq[(a + 2 * TPC) * nL]], B2);
         B0 += B2;
         B1 += B3;
       }
@@ -747,16 +801,18 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       for (int d = TPC >> 1; d >= 1; d >>= 1) Bv += __shfl_xor_sync(0xffffffffu, Bv, d);
       double u = 0.0;
       if (c < nL && p == 0) {
-        const double hl = s.hL[c];
+        const double hl = cL * s.hL1[c];  // renormalised hL_c of update t
         const double num = form == 0 ? hl * Bv * invN : Bv * rcp_fast(N * hl);
         u = (num + P.alpha * s.hSc[c]) * invDenL;
         u = u > 0.0 ? u : 0.0;
         s.hL1[c] = u;
+        s.hL2[c] = u * u;
       }
       PHASE(12);
       slot_put3(s, R_SL1, u, R_QL1, u * u, -1, 0.0, TPC);
     }
     PHASE(13);
+    SR1 = slot_sum<T>(s, R_SR1);
     __syncthreads();
     PHASE(3);
     if (kTrace) {  // after Eq. 12 (raw hR', raw hL')
@@ -764,10 +820,15 @@ __device__ __forceinline__ int iterate(Sm& s, const hr_params& P, int nR, int nL
       if (tid == 0 && 3 * t + 2 < trace_cap) trace[3 * t + 2] = F;
     }
     ++t;
-    SR1 = slot_sum<T>(s, R_SR1);
     SL1 = slot_sum<T>(s, R_SL1);
     QL1 = slot_sum<T>(s, R_QL1);
   }
+  {  // the renormalised final iterates (Eqs. 15, 14)
+    const double cR = N * rcp_fast(SR1), cL = N * rcp_fast(SL1);
+    if (tid < nR) s.hR[tid] = cR * s.hR1[tid];
+    if (tid < nL) s.hL[tid] = cL * s.hL1[tid];
+  }
+  __syncthreads();
 #ifdef HR_SOLVE_PROFILE
   if (blockIdx.x == kProfBlock && threadIdx.x == 0)
     for (int i = 0; i < 16; ++i) g_solve_clk[512 + i] = pacc[i];
@@ -844,12 +905,17 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   }
 
   // ---- initial state: hR^0 = hG, hL^0 = hS (R9), as raw iterates whose sums are N ----
+  double q0 = 0.0;
   if (tid < nL) {
     const double v = s.hSd[s.listL[tid]];
     s.hL1[tid] = v;
     s.hSc[tid] = v;
     s.hL[tid] = v;
+    s.hL2[tid] = v * v;
+    q0 = v * v;
   }
+  if (tid == 0) s.hL1[kLevels] = 0.0;         // the factor of unused chunk slots
+  slot_put3(s, R_QL1, q0, -1, 0.0, -1, 0.0);  // sum hS^2: the first Eq. 13's denominator
   if (tid < nR) {
     const double v = (double)s.hGi[s.listR[tid]];
     s.hR1[tid] = v;
@@ -870,7 +936,7 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   }
   __syncthreads();
   RunArena A;
-  run_build<T>(s, nR, nL, kc, mask, arenaS, AB, keysS, arenaG, A, wscr);
+  run_build<T>(s, nR, nL, kc, mask, arenaS, AB, keysS, arenaG, A, wscr, true);  // bin-ordered cell chunks
   PROF_MARK();
 
   double* tr = args.trace ? args.trace + b * (int64_t)args.trace_stride : nullptr;
@@ -912,7 +978,7 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   }
   const bool dS = keysS && align16(E) + 8 * Wtot <= AB - kMaskBytes;
   double* D = dS ? reinterpret_cast<double*>(arenaS + align16(E)) : reinterpret_cast<double*>(arenaG);
-  HR_CHECK(dS || 8 * Wtot <= 12 * kMaxPieces);
+  HR_CHECK(dS || 8 * Wtot <= kArenaRun);
   for (int i = tid; i < Wtot; i += T) D[i] = 0.0;
   __syncthreads();
   if (tid < nR) row_runs(kc1 + tid * nL, nL, s.hL, s.hR[tid], D, offr);  // row a = tid
