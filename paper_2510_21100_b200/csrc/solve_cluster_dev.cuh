@@ -124,14 +124,26 @@ __device__ int iterate_cluster(Sm& s, SmClusterExtra& x, cg::cluster_group& cl, 
         s.hL2[tid] = n * n;
         q = n * n;
       }
-      const uint32_t* __restrict__ pd = A.pDesc;
+      // one chunk of 8 bin-ordered local cells per thread (run_build with chunks)
+      const uint4* __restrict__ cd = reinterpret_cast<const uint4*>(A.pDesc);
       double* __restrict__ pv = A.pVal;
-      const double* __restrict__ hl1 = s.hL1;
-      const double* __restrict__ hr1 = s.hR1 + aB;
+      const unsigned char* __restrict__ hrb = reinterpret_cast<const unsigned char*>(s.hR1 + aB);
+      const unsigned char* __restrict__ hlb = reinterpret_cast<const unsigned char*>(s.hL1);
       for (int p = tid; p < A.P; p += T) {
-        const uint32_t d = pd[p];
-        HR_CHECK((int)(d >> 16) < nRl && (int)((d >> 8) & 255) < nL && (int)(d & 255) <= (int)((d >> 8) & 255));
-        pv[p] = hr1[d >> 16] * piece_sum(hl1, d & 255, (d >> 8) & 255) * cRL;
+        const uint4 q0 = cd[2 * p], q1 = cd[2 * p + 1];
+        const uint32_t d[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        double xv[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          HR_CHECK((int)(d[m] & 0xFFFFu) < 8 * (nRl > 0 ? nRl : 1) && (int)(d[m] >> 16) <= 8 * kLevels);
+          xv[m] = *reinterpret_cast<const double*>(hrb + (d[m] & 0xFFFFu)) *
+                  *reinterpret_cast<const double*>(hlb + (d[m] >> 16));
+        }
+#pragma unroll
+        for (int w = 1; w < 8; w <<= 1)
+#pragma unroll
+          for (int m = 0; m + w < 8; m += 2 * w) xv[m] += xv[m + w];
+        pv[p] = xv[0] * cRL;
       }
       if (t == 0 || P.use_epsilon) slot_put3(s, R_DR, dr, R_DL, dl, R_SL2, q);
     }
@@ -337,6 +349,7 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
     s.hSc[tid] = v;
     s.hL[tid] = v;
   }
+  if (tid == 0) s.hL1[kLevels] = 0.0;  // the factor of unused chunk slots
   if (tid < nR) {
     const double v = (double)s.hGi[s.listR[tid]];
     s.hR1[tid] = v;
@@ -368,7 +381,7 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
   CMARK(2);
   RunArena A;
   if (nRl > 0) {
-    run_build<T>(s, nRl, nL, kcR, mask, arenaS, AB - kcLb, true, arenaG, A, wscr);
+    run_build<T>(s, nRl, nL, kcR, mask, arenaS, AB - kcLb, true, arenaG, A, wscr, true);  // bin-ordered chunks
   } else {  // more ranks than rows: no local pieces
     A.P = 0;
     A.RR = 0;

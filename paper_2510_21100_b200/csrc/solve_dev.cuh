@@ -109,7 +109,8 @@ struct __align__(16) Sm {
   double red[kSlots][kMaxSW];
   uint32_t hSi[kLevels], hGi[kLevels];
   int keyStart[kLevels + 1];  // piece offsets per bin (bin order)
-  int pStart[kLevels], cBase[kLevels];  // run_build (chunks): a bin's first chunk / first cell
+  alignas(16) int pStart[kLevels];      // run_build (chunks): a bin's first chunk; Eq. 20: packed row ranges
+  int cBase[kLevels];                   // run_build (chunks): a bin's first cell
   uint8_t listR[kLevels], listL[kLevels];
   uint8_t binList[kLevels];   // the bins holding pieces, ascending (E2: lanes per bin)
   int nBins;
@@ -482,36 +483,40 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
 }
 
 // One row's Eq. 20 run sums (keys kr[0..nL) non-decreasing): D[off + k - k0] = hra * (sum of
-// hL over the row's cells of key k), in column order.  Keys and hL are loaded 8 cells at a time
-// (all in flight together) before the sequential pass over them, so the walk does not wait for a
-// load per cell; the additions are the plain column-order ones.
+// hL over the row's cells of key k), in column order.  Branch-free: every cell stores the
+// running sum of its run (the run's last cell stores the complete sum), so lanes walking
+// different rows do not diverge at their run boundaries; keys and hL are loaded 8 cells at a
+// time (all in flight together).  Entries of keys the row skips are not written (zeroed before).
 __device__ __forceinline__ void row_runs(const uint8_t* __restrict__ kr, int nL, const double* __restrict__ hL,
                                          double hra, double* __restrict__ D, int off) {
-  const int k0 = kr[0];
+  const int k0 = kr[0], klast = kr[nL - 1];
   double acc = 0.0;
-  int k = k0;
+  int kprev = k0;
+  D += off - k0;
   for (int c0 = 0; c0 < nL; c0 += 8) {
     int kk[8];
-    double hv[8];
+    double hv[8], g[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const bool in = c0 + m < nL;
-      kk[m] = in ? kr[c0 + m] : -1;
+      kk[m] = in ? (int)kr[c0 + m] : klast;  // a slot past the row's end continues the last run with + 0
       hv[m] = in ? hL[c0 + m] : 0.0;
+    }
+    // The issue is in order, so the batch has no branch and one dependent operation per cell:
+    // acc = acc * g + h with g = 0 where a run starts, else 1 (both exact), the flags computed
+    // from neighbouring keys ahead of the chain; the multiplies and stores follow independently.
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      HR_CHECK(kk[m] >= (m ? kk[m - 1] : kprev));
+      g[m] = kk[m] != (m ? kk[m - 1] : kprev) ? 0.0 : 1.0;
     }
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-      if (kk[m] < 0) break;
-      HR_CHECK(kk[m] >= k);
-      if (kk[m] != k) {
-        D[off + k - k0] = hra * acc;
-        acc = 0.0;
-        k = kk[m];
-      }
-      acc += hv[m];
+      acc = fma(acc, g[m], hv[m]);
+      D[kk[m]] = hra * acc;
     }
+    kprev = kk[7];
   }
-  D[off + k - k0] = hra * acc;
 }
 
 // sum of h[lo..hi] (hi - lo < kPiece): all loads predicated and in flight at once, fixed tree
@@ -938,6 +943,19 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   RunArena A;
   run_build<T>(s, nR, nL, kc, mask, arenaS, AB, keysS, arenaG, A, wscr, true);  // bin-ordered cell chunks
   PROF_MARK();
+  // the index_1 rows of the support rows (Eqs. 17-19 table) for Eq. 20: copied asynchronously
+  // into the (now dead) bin-mask region while the iterations run (nR <= 32: 8 KB)
+  const bool tabS = nR * kLevels <= kMaskBytes;
+  if (tabS) {
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(mask);
+    for (int i = tid; i < nR * (kLevels / 16); i += T) {
+      const int a = i >> 4, j = i & 15;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + a * kLevels + j * 16),
+                   "l"(args.idx1_tab + (size_t)s.listR[a] * kLevels + j * 16)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
 
   double* tr = args.trace ? args.trace + b * (int64_t)args.trace_stride : nullptr;
   const int t = tr ? (P.update_form == 0 ? iterate<T, true, 0>(s, P, nR, nL, N, kc, A, tr, args.trace_stride)
@@ -956,50 +974,74 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   // ---- Eq. 20: runs of index_1 (Eqs. 17-19) along each row, summed per bin in row order ----
   // index_1 of every cell from the per-gamma table (built once per gamma by k_idx1_table)
   uint8_t* kc1 = kc;
-  for (int e = tid; e < E; e += T) {
-    const int a = e / nL, c = e - a * nL;
-    kc1[e] = __ldg(args.idx1_tab + s.listR[a] * kLevels + s.listL[c]);
+  SLOT_MARK(10);
+  if (tabS) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const uint8_t* tab = reinterpret_cast<const uint8_t*>(mask);
+    for (int e = tid; e < E; e += T) {
+      const int a = e / nL, c = e - a * nL;
+      kc1[e] = tab[a * kLevels + s.listL[c]];
+    }
+  } else {
+    for (int e = tid; e < E; e += T) {
+      const int a = e / nL, c = e - a * nL;
+      kc1[e] = __ldg(args.idx1_tab + s.listR[a] * kLevels + s.listL[c]);
+    }
   }
   // index_1 is non-decreasing along a row (b_i p_j increases with j), so row a's keys cover the
   // range [kmin_a, kmax_a]; D holds, per row, hR_a * (sum of hL over the cells of key k) for k in
   // that range (zero where no cell has key k), rows at offsets rowOff[a] (a block scan of the
   // widths).  Then T_k = (1/N) sum over the rows, in row order, of D[a][k]: deterministic, and no
   // run/piece structure to build (that build cost more than the sums themselves).
-  int* rowOff = s.keyStart;                          // the iteration's bin offsets are dead now
-  uint8_t* kmin = reinterpret_cast<uint8_t*>(mask);  // so is the bin row mask
   __syncthreads();
-  SLOT_MARK(20);
+  SLOT_MARK(11);
   const int wr = tid < nR ? (int)kc1[tid * nL + nL - 1] - (int)kc1[tid * nL] + 1 : 0;
   int Wtot;
   const int offr = block_scan_excl<T>(wr, &Wtot, wscr);
-  if (tid < nR) {
-    rowOff[tid] = offr;
-    kmin[tid] = kc1[tid * nL];
-  }
+  // per row: kmin | kmax << 8 | offset << 16 (offset < Wtot <= 65536), padded to a multiple of 4
+  // rows with empty ranges (kmin > kmax)
+  uint32_t* rowPack = reinterpret_cast<uint32_t*>(s.pStart);
+  if (tid < ((nR + 3) & ~3))
+    rowPack[tid] = tid < nR ? (uint32_t)kc1[tid * nL] | ((uint32_t)kc1[tid * nL + nL - 1] << 8) | ((uint32_t)offr << 16)
+                            : 1u;
   const bool dS = keysS && align16(E) + 8 * Wtot <= AB - kMaskBytes;
   double* D = dS ? reinterpret_cast<double*>(arenaS + align16(E)) : reinterpret_cast<double*>(arenaG);
   HR_CHECK(dS || 8 * Wtot <= kArenaRun);
   for (int i = tid; i < Wtot; i += T) D[i] = 0.0;
   __syncthreads();
+  SLOT_MARK(12);
   if (tid < nR) row_runs(kc1 + tid * nL, nL, s.hL, s.hR[tid], D, offr);  // row a = tid
   __syncthreads();
+  SLOT_MARK(13);
   double* Tt = s.rho;  // dense target
-  if (binT) {
+  if (binT) {  // rows in order; four rows' ranges (one 16-B load) and entries in flight per step
     double e0 = 0.0;
-    for (int a = 0; a < nR; ++a) {
-      const int j = tid - (int)kmin[a];
-      const int w = (a + 1 < nR ? rowOff[a + 1] : Wtot) - rowOff[a];
-      if (j >= 0 && j < w) e0 += D[rowOff[a] + j];
+    const uint4* __restrict__ rp = reinterpret_cast<const uint4*>(rowPack);
+    for (int a = 0; a < nR; a += 4) {
+      const uint4 q = rp[a >> 2];
+      const uint32_t r[4] = {q.x, q.y, q.z, q.w};
+      double v[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int lo = r[m] & 255, hi = (r[m] >> 8) & 255;
+        v[m] = (tid >= lo && tid <= hi) ? D[(int)(r[m] >> 16) + tid - lo] : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) e0 += v[m];  // + 0 for the rows without this key
     }
     Tt[tid] = e0 / N;
   }
   __syncthreads();
+  SLOT_MARK(14);
   if (args.target && binT) args.target[b * kLevels + tid] = Tt[tid];
   __syncthreads();
   PROF_MARK();
+  SLOT_MARK(15);
   if (args.lut || args.status)
     cdf_lut<T>(s.hSi, Tt, s.hL1, s.wgt, s.hL2, wscr, args.lut ? args.lut + b * kLevels : nullptr,
             args.status ? args.status + b : nullptr);
+  SLOT_MARK(16);
 }
 
 

@@ -67,4 +67,4 @@ for cfg, nimg in (("C3", 64), ("C5", 64), ("C2", 1), ("C4", 1)):
                   str([round(r[5][i] / max(r[6], 1)) for i in ix]) for ix in ((7, 8, 9, 0), (14, 15, 10, 1), (4, 5, 6, 2),
                                                                               (11, 12, 13, 3))))
         print(f"      run_build steps [count+scan, desc, fix+mask, keyscan, slots, pieces+scan/write]: {r[7]}"
-              f"  eq20 build: {r[8]}")
+              f"  tail [idx1 keys, scan+zero, row walks, bin sums, target store, cdf+lut]: {r[8]}")
