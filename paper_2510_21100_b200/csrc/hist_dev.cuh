@@ -149,19 +149,16 @@ __device__ __forceinline__ void grad_row(uint32_t sb, uint32_t* ghi, uint32_t Lg
   }
 }
 
-// L2 prefetch of one image row (bulk async prefetch, no registers held): [row, row + bytes)
-// widened to 16-B alignment and clamped to the image end (aligned down), so it never leaves
-// the caller's buffer.  Issued a few rows ahead of the walk by the first thread of each row
-// group: the walk's own loads (one row ahead, registers) then hit L2 instead of DRAM.
+// L2 prefetch of the image rows a few rows ahead of the walk: the walk's own loads (one row
+// ahead, registers) then hit L2 instead of DRAM.
 #ifndef HR_HIST_PF
 #define HR_HIST_PF 2
 #endif
-__device__ __forceinline__ void prefetch_row_l2(const uint8_t* row, size_t bytes, uintptr_t img_end) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(row) & ~(uintptr_t)15;
-  uintptr_t e = (reinterpret_cast<uintptr_t>(row) + bytes + 15) & ~(uintptr_t)15;
-  if (e > img_end) e = img_end;
-  if (e > a)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+// One 128-B line per lane: the first ceil(rowBytes / 128) threads of a row group each prefetch one
+// line of the row (p = the line's address in the row the walk is at; lines past the image's end
+// are skipped), two instructions per row instead of a bulk-prefetch descriptor built by one lane.
+__device__ __forceinline__ void prefetch_line_l2(const uint8_t* p, uintptr_t img_end) {
+  if (reinterpret_cast<uintptr_t>(p) < img_end) asm volatile("prefetch.global.L2 [%0];" ::"l"(p) : "memory");
 }
 
 // Zero the counters (all NT threads; caller synchronises before use).
@@ -174,12 +171,13 @@ __device__ __forceinline__ void hist_zero(uint32_t* sm) {
 // halo row when `halo`), starting at p (the strip's first byte in row ya).  rowEnd: the strip's
 // last pixel is x = W - 1 (dx = 0 there, no neighbour load).  RPG + 1 row steps for every lane
 // (a warp-uniform trip count); lanes with nr == 0 only mask their counts.
-// pf: this thread prefetches its group's rows into L2, HR_HIST_PF rows ahead (p is then the
-// row start; img_end the 16-B aligned-down end of the image).
+// pfp (nullable): this thread prefetches one 128-B line of each of its group's rows into L2,
+// HR_HIST_PF rows ahead (pfp = its line in row ya; img_end = the end of the image).
 template <int G, int VEC>
 __device__ __forceinline__ void walk_strip(const uint8_t* __restrict__ p, size_t rowBytes, int RPG, int nr,
                                            bool halo, bool rowEnd, uint32_t sb, uint32_t* ghi, uint32_t Lv,
-                                           uint32_t Lg, bool pf = false, uintptr_t img_end = 0) {
+                                           uint32_t Lg, const uint8_t* pfp = nullptr, uintptr_t img_end = 0) {
+  const bool pf = pfp != nullptr;  // pfp: this thread's line of the group's first row
   uint32_t Vp[G], Dp[G];
 #pragma unroll
   for (int q = 0; q < G; ++q) Vp[q] = Dp[q] = 0u;
@@ -220,12 +218,13 @@ __device__ __forceinline__ void walk_strip(const uint8_t* __restrict__ p, size_t
   for (int i = 0; i < 3 * G; ++i) wa[i] = wb[i] = 0u;
   if (pf)
     for (int r = 1; r < HR_HIST_PF; ++r)
-      if (need(r)) prefetch_row_l2(p + r * rowBytes, rowBytes, img_end);
+      if (need(r)) prefetch_line_l2(pfp + r * rowBytes, img_end);
   if (need(0)) load_row(p, wa, na);
   for (int it = 0; it <= RPG; it += 2) {
     if (pf) {  // rows it + PF and it + PF + 1 (this step pair's loads are rows it + 1, it + 2)
-      if (need(it + HR_HIST_PF)) prefetch_row_l2(p + HR_HIST_PF * rowBytes, rowBytes, img_end);
-      if (need(it + HR_HIST_PF + 1)) prefetch_row_l2(p + (HR_HIST_PF + 1) * rowBytes, rowBytes, img_end);
+      if (need(it + HR_HIST_PF)) prefetch_line_l2(pfp + HR_HIST_PF * rowBytes, img_end);
+      if (need(it + HR_HIST_PF + 1)) prefetch_line_l2(pfp + (HR_HIST_PF + 1) * rowBytes, img_end);
+      pfp += 2 * rowBytes;
     }
     if (need(it + 1)) load_row(p + rowBytes, wb, nb);
     step(wa, na, it);
@@ -277,9 +276,11 @@ __device__ __forceinline__ void hist_segment(const uint8_t* __restrict__ img, in
       const int x0 = act ? s * SW : 0;
       const bool rowEnd = (s == SPf - 1) && (xt == W);  // last pixel of this strip is x = W-1
       const uint8_t* p = img + (size_t)(act ? ya : 0) * rowBytes + (size_t)x0 * 3;
-      // the first strip of each row group prefetches the group's whole rows into L2
-      const uintptr_t img_end = (reinterpret_cast<uintptr_t>(img) + (size_t)H * rowBytes) & ~(uintptr_t)15;
-      walk_strip<G, VEC>(p, rowBytes, RPG, nr, halo, rowEnd, sb, ghi, Lv, Lg, act && s == 0 && HR_HIST_PF > 0, img_end);
+      // the first strips of each row group prefetch the group's rows into L2, one 128-B line each
+      const uintptr_t img_end = reinterpret_cast<uintptr_t>(img) + (size_t)H * rowBytes;
+      const bool pfl = act && HR_HIST_PF > 0 && (size_t)s * 128 < rowBytes;
+      const uint8_t* pfp = pfl ? img + (size_t)ya * rowBytes + (size_t)s * 128 : nullptr;
+      walk_strip<G, VEC>(p, rowBytes, RPG, nr, halo, rowEnd, sb, ghi, Lv, Lg, pfp, img_end);
     }
   }
 
