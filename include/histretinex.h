@@ -252,10 +252,11 @@ hr_status hr_trace_bind(hr_ctx* ctx, void* records_dev, uint32_t* count_dev, uin
                     solves; streaming grids sized to the slots the resident solver
                     CTAs leave.  0/1: off (separate kernels); -1: auto = 2 when B >= 2
      "group_first_pct" grouped step with 2 groups: the first group's share of  default -1
-                    the batch in % (0: equal groups; -1: auto = 38 for B <= #SMs / 2,
-                    a short first histogram pass hiding the first solves under the
-                    second, C3 0.254 vs 0.261 ms; 90 for larger batches, the last
-                    group's few solves beside the first group's apply, C5 0.167 vs 0.177)
+                    the batch in % (0: equal groups; -1: auto = 47 for B <= #SMs / 2,
+                    the first solves hidden under the second histogram pass and the
+                    last group still the larger one, C3 0.233 vs 0.244 ms at 50; 90
+                    for larger batches, the last group's few solves beside the first
+                    group's apply, C5 0.154 vs 0.177 ms ungrouped)
      "apply_gs"     grouped step's apply: 1024-pixel chunks per warp in one CTA  default 8
                     ticket of the last group (>= 1)
      "apply_full_grid" grouped step's apply grid: 1 every slot (2 per SM; CTAs  default -1

@@ -39,9 +39,10 @@ struct hr_ctx {
                             // group k, the apply beside the last group's solves (0/1: off; -1: auto
                             // = 2 when B >= 2)
   int group_first_pct = -1; // grouped step, G = 2: first group's share of the images in % (0: equal
-                            // groups; -1: auto = 38 for B <= SMs / 2 -- a short hist(0) lets solve(0)
-                            // hide under the longer hist(1), C3 24 + 40 images 0.254 ms vs 32 + 32
-                            // 0.261 -- and 90 for larger batches -- the last group's few solves
+                            // groups; -1: auto = 47 for B <= SMs / 2 -- solve(0) hides under hist(1)
+                            // and the last group stays the larger one (the apply then takes every
+                            // slot): C3 30 + 34 images 0.2332 ms, 24 + 40 0.2370, 32 + 32 0.2436 --
+                            // and 90 for larger batches -- the last group's few solves
                             // overlap the first group's apply, C5 230 + 26 images 0.167 vs 0.177)
   int apply_gs = 8;         // grouped step's apply: 1024-px chunks per warp in a CTA ticket
   int apply_full_grid = -1; // grouped step's apply grid: 1 every slot, 0 the slots the last group's
@@ -603,7 +604,7 @@ hr_status hr_enhance_debug(hr_ctx* c, const uint8_t* in, int64_t B, int32_t H, i
     auto gstart = [&](int64_t k) -> int64_t {
       if (k <= 0) return 0;
       if (k >= G) return B;
-      const int pct = c->group_first_pct >= 0 ? c->group_first_pct : (B <= c->num_sms / 2 ? 38 : 90);
+      const int pct = c->group_first_pct >= 0 ? c->group_first_pct : (B <= c->num_sms / 2 ? 47 : 90);
       if (G == 2 && pct > 0) return std::min<int64_t>(B - 1, std::max<int64_t>(1, (B * pct + 50) / 100));
       return B * k / G;
     };
