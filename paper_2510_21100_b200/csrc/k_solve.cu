@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kLevels) k_remap(const uint32_t* graw, int32_t
 __global__ void __launch_bounds__(kLevels) k_match(const uint32_t* hist_s, const double* target, uint8_t* lut,
                                              int32_t* status) {
   __shared__ uint32_t hSi[kLevels];
-  __shared__ double Tt[kLevels], Pt[kLevels], Ct[kLevels], Cs[kLevels];
+  __shared__ __align__(16) double Tt[kLevels], Pt[kLevels], Ct[kLevels], Cs[kLevels];
   __shared__ int wscr[kLevels / 32];
   const int64_t b = blockIdx.x;
   hSi[threadIdx.x] = hist_s[b * kLevels + threadIdx.x];

@@ -392,6 +392,19 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
   }
   cluster_sync_all();  // every CTA's state is initialised before any remote store
   CMARK(3);
+  // the index_1 rows of the local rows (Eq. 20) copied asynchronously into the dead bin-mask
+  // region while the iterations run (as in solve_image)
+  const bool tabS = nRl * kLevels <= kMaskBytes;
+  if (tabS) {
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(mask);
+    for (int i = tid; i < nRl * (kLevels / 16); i += T) {
+      const int a = i >> 4, j = i & 15;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + a * kLevels + j * 16),
+                   "l"(args.idx1_tab + (size_t)s.listR[aB + a] * kLevels + j * 16)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
 
   const int t = P.update_form == 0 ? iterate_cluster<T, CS, 0>(s, x, cl, rank, P, nR, nL, aB, nRl, cB, nLl, N, kcR, kcL, A)
                                    : iterate_cluster<T, CS, 1>(s, x, cl, rank, P, nR, nL, aB, nRl, cB, nLl, N, kcR, kcL, A);
@@ -405,21 +418,30 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
 
   // ---- Eq. 20 on the local rows: dense per-row run sums (solve_dev.cuh), summed per bin ----
   uint8_t* kc1 = kcR;
-  for (int e = tid; e < El; e += T) {
-    const int al = e / nL, c = e - al * nL;
-    kc1[e] = __ldg(args.idx1_tab + s.listR[aB + al] * kLevels + s.listL[c]);
+  if (tabS) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const uint8_t* tab = reinterpret_cast<const uint8_t*>(mask);
+    for (int e = tid; e < El; e += T) {
+      const int al = e / nL, c = e - al * nL;
+      kc1[e] = tab[al * kLevels + s.listL[c]];
+    }
+  } else {
+    for (int e = tid; e < El; e += T) {
+      const int al = e / nL, c = e - al * nL;
+      kc1[e] = __ldg(args.idx1_tab + s.listR[aB + al] * kLevels + s.listL[c]);
+    }
   }
-  int* rowOff = s.keyStart;
-  uint8_t* kmin = reinterpret_cast<uint8_t*>(mask);
   __syncthreads();
   CMARK(6);
   const int wr = tid < nRl ? (int)kc1[tid * nL + nL - 1] - (int)kc1[tid * nL] + 1 : 0;
   int Wtot;
   const int offr = block_scan_excl<T>(wr, &Wtot, wscr);
-  if (tid < nRl) {
-    rowOff[tid] = offr;
-    kmin[tid] = kc1[tid * nL];
-  }
+  // per local row: kmin | kmax << 8 | offset << 16, padded to a multiple of 4 rows with empty ranges
+  uint32_t* rowPack = reinterpret_cast<uint32_t*>(s.pStart);
+  if (tid < ((nRl + 3) & ~3))
+    rowPack[tid] = tid < nRl ? (uint32_t)kc1[tid * nL] | ((uint32_t)kc1[tid * nL + nL - 1] << 8) | ((uint32_t)offr << 16)
+                             : 1u;
   const bool dS = align16(El) + 8 * Wtot <= AB - kMaskBytes - kcLb;
   HR_CHECK(dS || 8LL * Wtot <= kArenaGlobal);
   double* D = dS ? reinterpret_cast<double*>(arenaS + align16(El)) : reinterpret_cast<double*>(arenaG);
@@ -428,12 +450,20 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
   if (tid < nRl) row_runs(kc1 + tid * nL, nL, s.hL, s.hR[aB + tid], D, offr);  // local row tid
   __syncthreads();
   CMARK(7);
-  if (binT) {
+  if (binT) {  // local rows in order; four rows' ranges (one 16-B load) and entries in flight per step
     double e0 = 0.0;
-    for (int a = 0; a < nRl; ++a) {
-      const int j = tid - (int)kmin[a];
-      const int w = (a + 1 < nRl ? rowOff[a + 1] : Wtot) - rowOff[a];
-      if (j >= 0 && j < w) e0 += D[rowOff[a] + j];
+    const uint4* __restrict__ rp = reinterpret_cast<const uint4*>(rowPack);
+    for (int a = 0; a < nRl; a += 4) {
+      const uint4 q = rp[a >> 2];
+      const uint32_t r[4] = {q.x, q.y, q.z, q.w};
+      double v[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int lo = r[m] & 255, hi = (r[m] >> 8) & 255;
+        v[m] = (tid >= lo && tid <= hi) ? D[(int)(r[m] >> 16) + tid - lo] : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) e0 += v[m];
     }
     x.est[tid] = e0;
   }

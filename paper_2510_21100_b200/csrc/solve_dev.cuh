@@ -236,12 +236,24 @@ __device__ void cdf_lut(const uint32_t* hSi, const double* Tt, double* Pt, doubl
       acc = (m == 0) ? Tt[8 * tid] : acc + Tt[8 * tid + m];
       loc[m] = acc;
     }
-    // carry_l = carry_{l-1} + total_{l-1}, strictly sequential over lanes
-    double carry = 0.0;
-    for (int l = 0; l < 32; ++l) {
-      const double tot = __shfl_sync(0xffffffffu, acc, l);
-      if (l < tid) carry = carry + tot;  // carry for lane tid: sum in lane order
+    // carry_l = carry_{l-1} + total_{l-1}, strictly sequential over lanes: lane 0 adds the 32
+    // totals in order (loads first, then one dependent add per lane) -- Ct is free until the
+    // barrier below: [0, 32) the totals, [32, 64) the carries
+    Ct[tid] = acc;
+    __syncwarp();
+    if (tid == 0) {
+      double tot[32];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) tot[l] = Ct[l];
+      double c = 0.0;
+#pragma unroll
+      for (int l = 0; l < 32; ++l) {
+        Ct[32 + l] = c;
+        c = c + tot[l];
+      }
     }
+    __syncwarp();
+    const double carry = Ct[32 + tid];
 #pragma unroll
     for (int m = 0; m < 8; ++m) Pt[8 * tid + m] = (tid == 0) ? loc[m] : carry + loc[m];
   }
@@ -253,22 +265,27 @@ __device__ void cdf_lut(const uint32_t* hSi, const double* Tt, double* Pt, doubl
   int res = tid;
   if (bin && !degenerate) {
     const double x = Cs[tid];
-    // k* = first k with Ct[k] >= x
-    int lo = 0, hi = kLevels;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (Ct[mid] >= x) hi = mid; else lo = mid + 1;
-    }
-    const int ks = lo;  // <= 255 because Ct[255] == 1 >= x
+    // first k with Ct[k] >= y (Ct non-decreasing, Ct[255] >= y): a 16-ary search, two rounds of
+    // 16 independent loads instead of 8 dependent ones
+    auto lower = [&](double y) -> int {
+      int j = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) j += Ct[16 * i + 15] < y ? 1 : 0;
+      j = j < 15 ? j : 15;
+      const double2* seg = reinterpret_cast<const double2*>(Ct + 16 * j);
+      int n = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double2 v = seg[i];
+        n += (v.x < y ? 1 : 0) + (v.y < y ? 1 : 0);
+      }
+      return 16 * j + (n < 15 ? n : 15);
+    };
+    const int ks = lower(x);  // <= 255 because Ct[255] == 1 >= x
     res = ks;
     if (ks > 0) {
       const double cprev = Ct[ks - 1];
-      // first index of the plateau holding Ct[ks-1]
-      int l2 = 0, h2 = ks - 1;
-      while (l2 < h2) {
-        const int mid = (l2 + h2) >> 1;
-        if (Ct[mid] >= cprev) h2 = mid; else l2 = mid + 1;
-      }
+      const int l2 = lower(cprev);  // first index of the plateau holding Ct[ks-1] (<= ks - 1)
       const double d0 = fabs(cprev - x);
       const double d1 = fabs(Ct[ks] - x);
       if (d0 <= d1) res = l2;  // ties -> smallest k
