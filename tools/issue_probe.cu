@@ -20,7 +20,7 @@ __global__ void probe(long long* out, double* sink, int n, const double* gh) {
   double acc = 0;
   long long t0 = clock64();
   for (int it = 0; it < n; ++it) {
-    const uint4* cd = reinterpret_cast<const uint4*>(desc);
+    const uint4* cd = GENERIC ? reinterpret_cast<const uint4*>(gh ? (const void*)gh : (const void*)desc) : reinterpret_cast<const uint4*>(desc);
     const int p = tid;
     const uint4 q0 = cd[2 * p], q1 = cd[2 * p + 1];
     const uint32_t d[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
@@ -32,7 +32,7 @@ __global__ void probe(long long* out, double* sink, int n, const double* gh) {
     for (int w = 1; w < 8; w <<= 1)
 #pragma unroll
       for (int m = 0; m + w < 8; m += 2 * w) x[m] += x[m + w];
-    pv[p] = x[0] + acc;
+    (GENERIC ? (gh ? const_cast<double*>(gh) + 4096 : pv) : pv)[p] = x[0] + acc;
     __syncthreads();
     acc += pv[(p + 1) % T] * 1e-300;
   }
@@ -79,9 +79,10 @@ __global__ void probe(long long* out, double* sink, int n, const double* gh) {
 int main() {
   long long* d; double* s;
   cudaMalloc(&d, 64 * 8); cudaMalloc(&s, 1024 * 8);
-  for (int grid : {1, 148, 296})
-    for (int th : {32, 64, 128, 256, 512}) {
-      probe<false><<<grid, th>>>(d, s, 200, nullptr); probe<false><<<grid, th>>>(d, s, 200, nullptr);
+  for (int grid : {1, 2})
+    for (int th : {32, 96, 256}) {
+      if (grid == 1) { probe<false><<<1, th>>>(d, s, 200, nullptr); probe<false><<<1, th>>>(d, s, 200, nullptr); }
+      else { probe<true><<<1, th>>>(d, s, 200, nullptr); probe<true><<<1, th>>>(d, s, 200, nullptr); }
       cudaDeviceSynchronize();
       long long h[8]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
       printf("grid=%3d threads=%3d: chunk phase+bar %lld | gather walk+shfl+bar %lld | 64 dep IMAD %lld | 64 DFMA in 8 chains %lld cycles\n",
