@@ -7,12 +7,12 @@
 // readings R1-R21 exactly as in solve_dev.cuh.
 //
 // Split (rank r of CS): rows a in [aB, aE) = [nR r / CS, nR (r+1) / CS) for the E and R passes
-// (their keys index(i,j), runs and pieces are built from those rows only), columns c in
+// (their keys index(i,j), runs and cell chunks are built from those rows only), columns c in
 // [cB, cE) = [nL r / CS, nL (r+1) / CS) for the L pass (over all rows).  Every CTA keeps the
 // FULL state vectors (hR, hL, raw hR', hL', L-pass row weights) in its own shared memory.
 // One iteration:
 //   E1  renormalise the full raw iterates (Eqs. 15, 14; identical arithmetic in every CTA),
-//       piece sums of the local pieces
+//       chunk sums of the local cells
 //   E2  per bin, the local rows' EstRaw partial  -> cluster barrier
 //   E3  EstRaw_k = sum over ranks, in rank order, of the partials (DSMEM loads), rho_k
 //   R   Eq. 13 for the local rows; hR'_a and the L weight stored into EVERY CTA (DSMEM
@@ -107,7 +107,7 @@ __device__ int iterate_cluster(Sm& s, SmClusterExtra& x, cg::cluster_group& cl, 
 #endif
   CPH_T0();
   for (;;) {
-    // ======== E1: renormalise (Eqs. 15, 14), local piece sums (Eqs. 6, 8) ========
+    // ======== E1: renormalise (Eqs. 15, 14), local chunk sums (Eqs. 6, 8) ========
     const double cL = SL1 == N ? 1.0 : N * rcp_fast(SL1);
     const double cR = SR1 == N ? 1.0 : N * rcp_fast(SR1), cRL = cR * cL;
     {
@@ -381,8 +381,8 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
   CMARK(2);
   RunArena A;
   if (nRl > 0) {
-    run_build<T>(s, nRl, nL, kcR, mask, arenaS, AB - kcLb, true, arenaG, A, wscr, true);  // bin-ordered chunks
-  } else {  // more ranks than rows: no local pieces
+    run_build<T>(s, nRl, nL, kcR, mask, arenaS, AB - kcLb, true, arenaG, A, wscr);  // bin-ordered chunks
+  } else {  // more ranks than rows: no local chunks
     A.P = 0;
     A.RR = 0;
     A.pDesc = nullptr;

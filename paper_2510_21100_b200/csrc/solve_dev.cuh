@@ -22,15 +22,16 @@
 // Supports never change (hR stays 0 off supp(hG), hL off supp(hS)), so all work runs over the
 // nR x nL compacted cells only.
 //
-// Run structure.  index(i,j) is monotone in j, so each compacted row splits into a few RUNS
-// of equal output bin k (found once per image by a row walk).  EstRaw_k is the sum over the
-// runs of bin k of hR_a * (sum of hL over the run); a run's slot in the bin-ordered array is
-// fixed by a per-bin bitmask of rows (rank = popc of the bits below its row), so every
-// per-bin sum runs in row order: deterministic, no floating-point atomics, bit-identical run
-// to run.  The R- and L-updates are thread-per-row / thread-per-column walks (no combine).
-// The renormalisation of iteration t is folded into the run-sum phase of iteration t+1, so
-// an iteration is four phases / four barriers:  E1 (renorm + run sums) | E2 (EstRaw, rho)
-// | R (Eq. 13) | L (Eq. 12).  Eq. 20 reuses the run machinery with index_1.
+// Chunk structure.  index(i,j) is monotone in j, so each compacted row splits into a few RUNS
+// of equal output bin k.  The cells are laid out in BIN order (bin, then row, then column; a
+// run's place among its bin's runs is fixed by a per-bin bitmask of rows: rank = popc of the
+// bits below its row) and cut into chunks of 8 cells that never straddle a bin.  EstRaw_k is the
+// sum of the bin's chunk sums in that order: deterministic, no floating-point atomics,
+// bit-identical run to run.  The R- and L-updates are walks over a row / a column by 1-8 lanes.
+// The iterates stay raw; the renormalisation factors of Eqs. 15, 14 are scalars applied where a
+// renormalised value enters, so an iteration is four phases / four barriers:
+//   E1 (chunk sums of the cell products) | E2 (EstRaw, rho) | R (Eq. 13) | L (Eq. 12).
+// Eq. 20 sums hR_a hL_c per index_1 key by dense per-row run sums (no second chunk structure).
 #pragma once
 #include "hr_common.cuh"
 
@@ -41,30 +42,23 @@ namespace {
 // (few images: one CTA per SM, the cell loops spread over twice the warps).  Bin-indexed steps
 // use threads 0..255 (thread k <-> bin k); the others only join the cell loops and barriers.
 constexpr int kMaxSW = 16;  // warps of the widest solver CTA
-// Run arena (per image): runs = maximal equal-key segments of a compacted row; pieces = runs
-// cut into at most kPiece cells (bounds the per-thread sum chains of the E1 phase).  Pieces
-// are stored in BIN order (bin, then row, then position), so a bin's pieces are contiguous:
-//   pDesc [P] u32   lo | hi << 8 | a << 16       (persistent)
-//   pVal  [P] f64   piece values                  (persistent; build scratch before that:
-//                   runDesc [RR] u32 row order k | lo << 8 | hi << 16 | a << 24, and the
-//                   bin-ordered per-run piece counts / offsets [RR] u32)
-//   s.keyStart[k] = first piece of bin k
-#ifndef HR_KPIECE
-#define HR_KPIECE 8
-#endif
-constexpr int kPiece = HR_KPIECE;
-static_assert(kPiece == 8 || kPiece == 16, "piece length");
+// Chunk arena (per image): runs = maximal equal-key segments of a compacted row; the cells in BIN
+// order (bin, then row, then column), kChunk per chunk, a bin's last chunk padded:
+//   pDesc [8 P] u32  per cell: (byte offset of hR1_a) | (byte offset of hL1_c) << 16; an unused
+//                    slot points at hL1[256] = 0                                  (persistent)
+//   pVal  [P] f64    chunk sums                   (persistent; build scratch before that:
+//                    runDesc [RR] u32 row order k | lo << 8 | hi << 16 | a << 24, and the
+//                    bin-ordered per-run cell counts / offsets [RR] u32)
+//   s.keyStart[k] = first chunk of bin k
 constexpr int kMaxRuns = 32896;                        // sum_{i<256} (i + 1): runs of any image
-constexpr int kMaxPieces = kMaxRuns + 65536 / kPiece;  // P <= RR + E / kPiece
-constexpr int kChunk = 8;                              // cells per chunk (k_solve: bin-ordered chunks)
+constexpr int kChunk = 8;                              // cells per chunk
 constexpr int kMaxChunks = 65536 / kChunk + 256;       // each bin's last chunk may be partial
 constexpr int kMaskBytes = kLevels * 8 * 4;            // per-bin row bitmask (8 words per bin)
 constexpr int kArenaSmem = 80 * 1024;  // default shared arena: keys (E bytes) + run arena + mask tail
 constexpr int kKeysGlobal = 65536;      // keys of images whose keys do not fit the shared arena
-// per-image global arena: descriptors + max(values, build scratch) of either form, then keys
+// per-image global arena: descriptors + max(values, build scratch), then keys
 constexpr int kArenaRun = 4 * kChunk * kMaxChunks + 8 * kMaxRuns + 256;
 constexpr int kArenaGlobal = kArenaRun + kKeysGlobal;
-static_assert(kArenaRun >= 12 * kMaxPieces + 256, "the piece form fits too");
 
 // Phase clock marks (measurement builds only: -DHR_SOLVE_PROFILE; block kProfBlock, thread 0).
 #ifdef HR_SOLVE_PROFILE
@@ -108,11 +102,11 @@ struct __align__(16) Sm {
   double bk[kLevels];                 // b_k = k/255 (R1)
   double red[kSlots][kMaxSW];
   uint32_t hSi[kLevels], hGi[kLevels];
-  int keyStart[kLevels + 1];  // piece offsets per bin (bin order)
+  int keyStart[kLevels + 1];  // chunk offsets per bin (bin order)
   alignas(16) int pStart[kLevels];      // run_build (chunks): a bin's first chunk; Eq. 20: packed row ranges
   int cBase[kLevels];                   // run_build (chunks): a bin's first cell
   uint8_t listR[kLevels], listL[kLevels];
-  uint8_t binList[kLevels];   // the bins holding pieces, ascending (E2: lanes per bin)
+  uint8_t binList[kLevels];   // the bins holding chunks, ascending (E2: lanes per bin)
   int nBins;
   unsigned long long nw[kMaxSW];
 };
@@ -337,25 +331,24 @@ struct RunArena {
   int RR, P;
 };
 
-// Run + piece structure of the keys keys[a * nL + c] (non-decreasing in c), built in
+// Run + chunk structure of the keys keys[a * nL + c] (non-decreasing in c), built in
 // parallel over cells: thread t owns cells [E t / T, E (t+1) / T).  A cell starts a run when
 // c == 0 or its key differs from the left neighbour; a block scan numbers the runs in row
 // order.  Each run sets its row's bit in the bin's mask (atomicOr: the result is order-free);
 // its bin-ordered slot = (runs of smaller bins) + rank of its row among the bin's rows.  A
-// scan of the per-slot piece counts places every piece in bin order.  Placement: after the
-// keys in shared memory when it fits (mask tail excluded), else arenaG.
-// chunks (k_solve): instead of pieces of a run, the CELLS are laid out in bin order (bin, then
-// row, then column) and cut into chunks of kChunk cells that never straddle a bin (a bin's last
-// chunk is padded with slots whose factor is hL1[256] = 0): chunk p = pDesc[8p .. 8p + 8), a cell
-// = (byte offset of hR1_a) | (byte offset of hL1_c) << 16; s.keyStart = chunk offsets per bin.
-// The E1 phase is then one chunk (8 independent products, a fixed tree) per thread with ~E / 8 +
-// (bins) chunks in all -- row-run pieces are mostly 1-2 cells long when the rows are sparse (a
-// MAXNORM gradient support), so there were ~5 per thread.
+// scan of the per-slot run lengths gives every run's first cell in bin order, a scan of the
+// bins' chunk counts each bin's first chunk: the CELLS are written in bin order (bin, then row,
+// then column), kChunk per chunk, chunks never straddling a bin (a bin's last chunk is padded
+// with slots whose factor is hL1[256] = 0): chunk p = pDesc[8p .. 8p + 8), a cell = (byte offset
+// of hR1_a) | (byte offset of hL1_c) << 16; s.keyStart = chunk offsets per bin.  The E1 phase is
+// then one chunk (8 independent products, a fixed tree) per thread with ~E / 8 + (bins) chunks
+// in all -- pieces of single runs are mostly 1-2 cells long when the rows are sparse (a MAXNORM
+// gradient support): ~5 per thread on C3.  Placement: after the keys in shared memory when it
+// fits (mask tail excluded), else arenaG.
 template <int T>
 __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* mask, unsigned char* arenaS,
                           int arenaBytes, bool keysInSmem, unsigned char* arenaG, RunArena& A, int* wscr,
-                          bool chunks = false, int pslot = 0) {
-  constexpr int plen = kPiece;
+                          int pslot = 0) {
   const int tid = threadIdx.x;
   SLOT_MARK(pslot + 0);
   const int E = nR * nL;
@@ -375,18 +368,18 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   int RR;
   int r = block_scan_excl<T>(cnt, &RR, wscr);
   SLOT_MARK(pslot + 1);
-  const int Pmax = chunks ? E / kChunk + kLevels : RR + E / plen;
+  const int Pmax = E / kChunk + kLevels;
   HR_CHECK(RR >= nR && RR <= E && RR <= kMaxRuns);
   const int keysS = keysInSmem ? align16(E) : 0;
-  const int descB = align16(chunks ? 4 * kChunk * Pmax : 4 * Pmax);
-  const int valB = 8 * (Pmax > RR ? Pmax : RR);  // piece values; the build scratch before that
+  const int descB = align16(4 * kChunk * Pmax);
+  const int valB = 8 * (Pmax > RR ? Pmax : RR);  // chunk sums; the build scratch before that
   const bool sm = keysS + descB + valB <= arenaBytes - kMaskBytes;
   unsigned char* base = sm ? arenaS + keysS : arenaG;
   A.pDesc = reinterpret_cast<uint32_t*>(base);
   A.pVal = reinterpret_cast<double*>(base + descB);
   A.RR = RR;
   uint32_t* runDesc = reinterpret_cast<uint32_t*>(A.pVal);  // build scratch under pVal
-  uint32_t* slotN = runDesc + RR;                           // bin order: pieces, then offsets
+  uint32_t* slotN = runDesc + RR;                           // bin order: cell counts, then offsets
   {  // descriptors with hi provisional (fixed below)
     int a = e0 / nL, c = e0 - a * nL;
     int prev = (e0 < e1 && c > 0) ? keys[e0 - 1] : -1;
@@ -424,16 +417,16 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
   const int kfirst = block_scan_excl<T>(kcount, &RK, wscr);  // first run slot of bin tid
   if (tid < kLevels) s.keyStart[tid] = kfirst;
   __syncthreads();
-  for (int q = r0; q < r1; ++q) {  // piece count at the run's bin-order slot
+  for (int q = r0; q < r1; ++q) {  // cell count at the run's bin-order slot
     const uint32_t d = runDesc[q];
     const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
     HR_CHECK(lo <= hi && hi < nL && a < nR);
     HR_CHECK(s.keyStart[k] + mask_rank(mask + k * 8, a) < RR);
-    slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)] = (uint32_t)(chunks ? hi - lo + 1 : (hi - lo) / plen + 1);
+    slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)] = (uint32_t)(hi - lo + 1);
   }
   __syncthreads();
   SLOT_MARK(pslot + 4);
-  int np = 0;  // exclusive scan of the bin-ordered piece counts -> piece offsets
+  int np = 0;  // exclusive scan of the bin-ordered cell counts -> cell offsets
   for (int q = r0; q < r1; ++q) np += (int)slotN[q];
   int P;
   int off = block_scan_excl<T>(np, &P, wscr);
@@ -443,10 +436,10 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     off += n;
   }
   A.P = P;
-  HR_CHECK(RK == RR && (chunks ? P == E : P >= RR && P <= Pmax));
+  HR_CHECK(RK == RR && P == E);
   __syncthreads();
   SLOT_MARK(pslot + 5);
-  if (chunks) {
+  {
     // cells per bin -> chunks per bin -> chunk offsets (a scan over the bins)
     int nc = 0, cs = 0;
     if (tid < kLevels) {
@@ -474,21 +467,9 @@ __device__ void run_build(Sm& s, int nR, int nL, const uint8_t* keys, uint32_t* 
     if (tid < kLevels) s.keyStart[tid] = s.pStart[tid];  // run slots -> chunk offsets
     if (tid == 0) s.keyStart[kLevels] = PC;
     A.P = PC;
-  } else {
-    for (int q = r0; q < r1; ++q) {  // pieces of each run at its bin-order offset
-      const uint32_t d = runDesc[q];
-      const int a = d >> 24, lo = (d >> 8) & 255, hi = (d >> 16) & 255, k = d & 255;
-      int p = (int)slotN[s.keyStart[k] + mask_rank(mask + k * 8, a)];
-      for (int l = lo; l <= hi; l += plen, ++p)
-        A.pDesc[p] = (uint32_t)l | ((uint32_t)min(l + plen - 1, hi) << 8) | ((uint32_t)a << 16);
-      HR_CHECK(p <= P);
-    }
-    __syncthreads();
-    if (tid < kLevels) s.keyStart[tid] = kfirst < RK ? (int)slotN[kfirst] : P;  // run slots -> piece offsets
-    if (tid == 0) s.keyStart[kLevels] = P;
   }
   __syncthreads();
-  {  // the bins holding pieces, ascending
+  {  // the bins holding chunks, ascending
     const bool has = tid < kLevels && s.keyStart[tid] < s.keyStart[tid + 1];
     int nb;
     const int pos = block_scan_excl<T>(has ? 1 : 0, &nb, wscr);
@@ -536,22 +517,8 @@ __device__ __forceinline__ void row_runs(const uint8_t* __restrict__ kr, int nL,
   }
 }
 
-// sum of h[lo..hi] (hi - lo < kPiece): all loads predicated and in flight at once, fixed tree
-__device__ __forceinline__ double piece_sum(const double* __restrict__ h, int lo, int hi) {
-  const int n = hi - lo;
-  double x[kPiece];
-#pragma unroll
-  for (int m = 0; m < kPiece; ++m) x[m] = (m <= n) ? h[lo + m] : 0.0;
-#pragma unroll
-  for (int w = 1; w < kPiece; w <<= 1)  // pairwise tree: ((x0 + x1) + (x2 + x3)) + ...
-#pragma unroll
-    for (int m = 0; m + w < kPiece; m += 2 * w) x[m] += x[m + w];
-  return x[0];
-}
-
-// sum over bin k of its pieces (contiguous, bin order: runs in row order)
-// (eight accumulators, eight loads in flight per step: the longest bin's chain -- bin 0 of a
-// dark image holds ~60 pieces -- sets the phase time)
+// sum over bin k of its chunk sums (contiguous, bin order; the cluster solver's E2)
+// (eight accumulators, eight loads in flight per step)
 __device__ __forceinline__ double bin_sum(const Sm& s, const RunArena& A, int k) {
   double e[8];
 #pragma unroll
@@ -958,7 +925,7 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   }
   __syncthreads();
   RunArena A;
-  run_build<T>(s, nR, nL, kc, mask, arenaS, AB, keysS, arenaG, A, wscr, true);  // bin-ordered cell chunks
+  run_build<T>(s, nR, nL, kc, mask, arenaS, AB, keysS, arenaG, A, wscr);  // bin-ordered cell chunks
   PROF_MARK();
   // the index_1 rows of the support rows (Eqs. 17-19 table) for Eq. 20: copied asynchronously
   // into the (now dead) bin-mask region while the iterations run (nR <= 32: 8 KB)
@@ -1010,7 +977,7 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   // range [kmin_a, kmax_a]; D holds, per row, hR_a * (sum of hL over the cells of key k) for k in
   // that range (zero where no cell has key k), rows at offsets rowOff[a] (a block scan of the
   // widths).  Then T_k = (1/N) sum over the rows, in row order, of D[a][k]: deterministic, and no
-  // run/piece structure to build (that build cost more than the sums themselves).
+  // second chunk structure to build (that build cost more than the sums themselves).
   __syncthreads();
   SLOT_MARK(11);
   const int wr = tid < nR ? (int)kc1[tid * nL + nL - 1] - (int)kc1[tid * nL] + 1 : 0;
