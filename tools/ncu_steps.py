@@ -31,18 +31,14 @@ def short(name):
 
 
 def steps(ls):
-    """Split at each run of three consecutive k_zero launches (the start of a step)."""
-    st, cur, i = [], [], 0
-    while i < len(ls):
-        if short(ls[i]["name"]).startswith("k_zero") and i + 2 < len(ls) and all(
-                short(ls[i + j]["name"]).startswith("k_zero") for j in range(3)):
-            if cur:
-                st.append(cur)
-            cur = ls[i:i + 3]
-            i += 3
-            continue
-        cur.append(ls[i])
-        i += 1
+    """Split at each k_zero launch that follows a non-k_zero launch (the start of a step)."""
+    st, cur = [], []
+    for i, k in enumerate(ls):
+        z = short(k["name"]).startswith("k_zero")
+        if z and cur and not short(ls[i - 1]["name"]).startswith("k_zero"):
+            st.append(cur)
+            cur = []
+        cur.append(k)
     if cur:
         st.append(cur)
     return st
