@@ -2,10 +2,16 @@
 #include <cstdio>
 #include "../paper_2510_21100_b200/csrc/solve_dev.cuh"
 using namespace hr;
-__global__ void probe(long long* out, uint8_t* lut, int rep) {
+__global__ void probe(long long* out, uint8_t* lut, int rep, double* gscratch) {
   __shared__ uint32_t hSi[256];
-  __shared__ __align__(16) double Tt[256], Pt[256], Ct[256], Cs[256];
+  __shared__ __align__(16) double Tt_[256], Pt_[256], Ct_[256], Cs_[256];
   __shared__ int wscr[8];
+  // gscratch == nullptr at run time, but the compiler cannot know: the arrays are reached through
+  // generic pointers, as in k_solve (state struct carved from dynamic shared memory)
+  double* Tt = gscratch ? gscratch : Tt_;
+  double* Pt = gscratch ? gscratch + 256 : Pt_;
+  double* Ct = gscratch ? gscratch + 512 : Ct_;
+  double* Cs = gscratch ? gscratch + 768 : Cs_;
   const int tid = threadIdx.x;
   hSi[tid] = tid < 80 ? 1000 + 37 * tid : 0;
   Tt[tid] = tid < 200 ? 1.0 + 0.01 * tid * tid : 0.0;
@@ -21,7 +27,7 @@ __global__ void probe(long long* out, uint8_t* lut, int rep) {
 int main() {
   long long* d; uint8_t* l;
   cudaMalloc(&d, 64 * 8); cudaMalloc(&l, 256);
-  probe<<<1, 256>>>(d, l, 20); probe<<<1, 256>>>(d, l, 20);
+  probe<<<1, 256>>>(d, l, 20, nullptr); probe<<<1, 256>>>(d, l, 20, nullptr);
   cudaDeviceSynchronize();
   long long h[8]; cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   uint8_t hl[256]; cudaMemcpy(hl, l, 256, cudaMemcpyDeviceToHost);
