@@ -5,20 +5,19 @@
 // (S is the HSV value channel): V = max(R,G,B), V' = LUT[V]; replacing V in hexcone HSV
 // scales every channel by V'/V (reading R17), rounded half up:
 //     out_c = floor((2 c V' + V) / (2 V)),  V = 0 -> (V', V', V').
-// Exact integer form: out_c = umulhi(c * e + V, M[V]) + (e >> 16) with the per-level entry
-//     V >= 1: e = 2 LUT[V],  M = floor(2^32 / (2V)) + 1   (exact for every numerator <= 130305)
-//     V == 0: e = LUT[0] << 16 (then c = 0, the numerator is 0 and the addend gives LUT[0]),
-// i.e. one IMAD and one IMAD.HI (with addend) per channel.
+// The streaming kernel evaluates it in fp32, out_c = rn(c alpha + beta) with alpha = fl(V'/V) and
+// beta = fl(1/(4V)) per level (exact: apply_dev.cuh); the scalar fallback kernel in integers,
+// out_c = umulhi(c * e + V, M[V]) + (e >> 16), e = 2 LUT[V], M = floor(2^32 / (2V)) + 1.
 //
-// B200 design: every warp runs its own TMA bulk-copy pipeline over 512-pixel chunks
-// (1,536 B): cp.async.bulk global->smem completes on a per-stage mbarrier, the 32 lanes
-// transform their 16 pixels in place (three conflict-free 16-B LDS/STS at a 48-B lane
-// stride), and cp.async.bulk smem->global writes whole lines back -- no partial-sector
-// stores (the v1 per-thread 48-B STG pattern sent 1.4x the bytes to L2).  M lives in a
-// lane-private table (word 32v + lane: conflict-free), (A | Bv << 16) in a per-warp table
-// rebuilt when the warp's chunk changes image, so warps never synchronise with each other.
-// Chunks never straddle images; images whose pixel count is not a multiple of 16 (or
-// unaligned buffers) take the scalar fallback kernel.
+// B200 design: every warp runs its own TMA bulk-copy pipeline over 1024-pixel chunks
+// (3,072 B): cp.async.bulk global->smem completes on a per-stage mbarrier, the 32 lanes
+// transform the chunk in place as two 512-px sub-blocks (lane l owns 16 px of each: three
+// conflict-free 16-B LDS/STS at a 48-B lane stride), and cp.async.bulk smem->global writes whole
+// lines back -- no partial-sector stores (the v1 per-thread 48-B STG pattern sent 1.4x the
+// bytes to L2).  Per pixel one 8-B LDS fetches (alpha, beta) from a per-warp table rebuilt when
+// the warp's chunk changes image, so warps never synchronise with each other.  Chunks never
+// straddle images; images whose pixel count is not a multiple of 16 (or unaligned buffers) take
+// the scalar fallback kernel.
 #include "apply_dev.cuh"
 
 namespace hr {
@@ -62,30 +61,65 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
   int64_t cur_img = -1;
   uint32_t nIss = 0, nComp = 0;  // chunks issued / computed by this warp so far (stage and parity)
 
-  auto where = [&](uint32_t g, uint64_t& off, uint32_t& bytes, uint32_t& b) {
-    b = g / cpi;
-    const uint32_t px0 = (g - b * cpi) * kChunkPx;
+  // A chunk cursor: image b and chunk li within it.  A warp's chunks are kWarps apart, so a cursor
+  // advances by an add and a compare (no division per chunk); every lane keeps the same cursors
+  // and counters (warp-uniform bookkeeping), lane 0 alone issues the bulk copies.
+  struct Cur {
+    uint32_t b, li;
+  };
+  auto cur_at = [&](uint32_t g) {
+    Cur c;
+    c.b = g / cpi;
+    c.li = g - c.b * cpi;
+    return c;
+  };
+  auto cur_step = [&](Cur& c) {
+    c.li += (uint32_t)kWarps;
+    while (c.li >= cpi) {
+      c.li -= cpi;
+      ++c.b;
+    }
+  };
+  auto span = [&](const Cur& c, uint64_t& off, uint32_t& bytes) {
+    const uint32_t px0 = c.li * kChunkPx;
     const uint32_t npx = min((uint32_t)kChunkPx, (uint32_t)(HW - px0));
-    off = ((uint64_t)b * (uint64_t)HW + px0) * 3u;
+    off = ((uint64_t)c.b * (uint64_t)HW + px0) * 3u;
     bytes = npx * 3u;
   };
-  auto issue = [&](uint32_t g) {  // lane 0
+  auto issue = [&](const Cur& c) {  // every lane: the stage bookkeeping; lane 0: the copy
     uint64_t off;
-    uint32_t bytes, b;
-    where(g, off, bytes, b);
+    uint32_t bytes;
+    span(c, off, bytes);
     const int st = (int)(nIss % kStages);
-    mbar_expect_tx(&s.bar[w][st], bytes);
-    bulk_load(s.stage[w][st], in + off, bytes, &s.bar[w][st], pol);
+    if (lane == 0) {
+      mbar_expect_tx(&s.bar[w][st], bytes);
+      bulk_load(s.stage[w][st], in + off, bytes, &s.bar[w][st], pol);
+    }
     ++nIss;
   };
-  // this warp's per-chunk pipeline over `count` chunks, chunk i = global chunk index chunk(i)
-  auto pipeline = [&](int count, auto&& chunk) {
-    if (lane == 0)
-      for (int i = 0; i < min(kAhead, count); ++i) issue(chunk(i));
-    for (int i = 0; i < count; ++i) {
+  // this warp's per-chunk pipeline over two runs of chunks: gA, gA + kWarps, ... (nA_ chunks),
+  // then gB, gB + kWarps, ... (nB_ chunks)
+  auto pipeline = [&](uint32_t gA, int nA_, uint32_t gB, int nB_) {
+    const int count = nA_ + nB_;
+    if (count <= 0) return;
+    Cur ci = cur_at(nA_ > 0 ? gA : gB), cc = ci;  // issue cursor (kAhead ahead), compute cursor
+    int ii = 0;                                   // index of the issue cursor's chunk
+    auto advance = [&](Cur& c, int& idx) {
+      ++idx;
+      if (idx == nA_ && nB_ > 0)
+        c = cur_at(gB);
+      else
+        cur_step(c);
+    };
+    for (int i = 0; i < min(kAhead, count); ++i) {
+      issue(ci);
+      advance(ci, ii);
+    }
+    for (int i = 0; i < count;) {
       uint64_t off;
-      uint32_t bytes, b;
-      where(chunk(i), off, bytes, b);
+      uint32_t bytes;
+      span(cc, off, bytes);
+      const uint32_t b = cc.b;
       if ((int64_t)b != cur_img) {  // per-warp LUT table for this image
         __syncwarp();
         if (ready && lane == 0) wait_flag_geq(ready + b, 1u, 100);
@@ -97,9 +131,10 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
       // prefetch chunk i + kAhead into the stage of chunk i - 2, whose bulk store (committed
       // two iterations ago) has finished reading shared memory once all but the latest
       // store group have
-      if (lane == 0 && i + kAhead < count) {
-        if (nComp >= 2) bulk_wait_read<1>();
-        issue(chunk(i + kAhead));
+      if (ii < count) {
+        if (lane == 0 && nComp >= 2) bulk_wait_read<1>();
+        issue(ci);
+        advance(ci, ii);
       }
       HR_CHECK(bytes > 0 && bytes <= (uint32_t)kChunkBytes && bytes % 48 == 0 && off + bytes <= (uint64_t)B * HW * 3);
       const int st = (int)(nComp % kStages);
@@ -113,26 +148,33 @@ k_apply_tma(const uint8_t* __restrict__ in, const uint8_t* __restrict__ lut, int
         bulk_commit();
       }
       ++nComp;
+      advance(cc, i);
     }
     if (lane == 0) bulk_wait_read<0>();  // the stages are free for the next call's prologue
     __syncwarp();
   };
 
-  // static shares: part A, then (without tickets) part B
-  pipeline(nA + cnt(c0, c1), [&](int i) {
-    return i < nA ? a0 + (uint32_t)w + (uint32_t)i * kWarps : c0 + (uint32_t)w + (uint32_t)(i - nA) * kWarps;
-  });
-  if (dynB) {  // part B by CTA tickets
-    const uint32_t CT = (uint32_t)kWarps * GS, nT = (GB + CT - 1) / CT;
-    for (;;) {
+  // round 0: the static shares (part A, then -- without tickets -- part B); further rounds: part B
+  // by CTA tickets.  One call site, so the pipeline body exists once in the kernel (the code of a
+  // step timed after an L2 flush is fetched from DRAM).
+  const uint32_t CT = (uint32_t)kWarps * GS, nT = dynB ? (GB + CT - 1) / CT : 0u;
+  for (int round = 0;; ++round) {
+    uint32_t gA_ = a0 + (uint32_t)w, gB_ = c0 + (uint32_t)w;
+    int nA_ = nA, nB_ = cnt(c0, c1);
+    if (round > 0) {
+      if (!dynB) break;
       __syncthreads();
       if (tid == 0) tk_s = atomicAdd(ticket, 1u);
       __syncthreads();
       const uint32_t t = tk_s;
       if (t >= nT) break;
       const uint32_t lo = GA + t * CT, hi = min(GA + GB, lo + CT);
-      pipeline(cnt(lo, hi), [&](int i) { return lo + (uint32_t)w + (uint32_t)i * kWarps; });
+      gA_ = lo + (uint32_t)w;
+      nA_ = cnt(lo, hi);
+      gB_ = 0u;
+      nB_ = 0;
     }
+    pipeline(gA_, nA_, gB_, nB_);
   }
   if (lane == 0) bulk_wait<0>();
   TRACE_END(4u, 0u, 0ull);
