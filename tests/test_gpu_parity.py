@@ -285,6 +285,23 @@ def test_apply_exhaustive_pixels():
         assert np.array_equal(out[0, 0], ref)
 
 
+def test_apply_every_level_triple():
+    """Every (V, c <= V, V') triple through the streaming kernel: image k holds one pixel (c, V, c)
+    per pair c <= V (32,896 pixels, a multiple of 16) and uses the LUT V -> (V + k) mod 256, so the
+    256 images cover every matched level for every (V, c) -- the fp32 colour quotient of
+    apply_dev.cuh against the exact hexcone oracle, 8.4 M triples."""
+    V, c = np.meshgrid(np.arange(256), np.arange(256), indexing="ij")
+    m = c <= V
+    px = np.stack([c[m], V[m], c[m]], -1).astype(np.uint8)           # (32896, 3)
+    assert px.shape[0] % 16 == 0
+    x = np.broadcast_to(px[None, None], (256, 1, px.shape[0], 3)).copy()
+    lut = ((np.arange(256)[None, :] + np.arange(256)[:, None]) % 256).astype(np.uint8)
+    out = hr().hr_apply(to_dev(x), to_dev(lut)).cpu().numpy()
+    for k in range(256):
+        ref = oracle.reconstruct(px, lut[k][px.max(-1)].astype(np.int32))
+        assert np.array_equal(out[k, 0], ref), k
+
+
 def test_apply_in_place_and_ragged():
     x = synth.make_image(37, 101, seed=9)[None]
     lut = np.arange(256, dtype=np.uint8)[::-1].copy()
