@@ -369,13 +369,11 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
   HR_CHECK(El <= AB - kMaskBytes - kcLb && kcLb + kMaskBytes <= AB);
   uint8_t* kcR = arenaS;
   uint8_t* kcL = arenaS + AB - kMaskBytes - kcLb;
-  for (int e = tid; e < El; e += T) {
-    const int al = e / nL, c = e - al * nL;
-    kcR[e] = (uint8_t)idx0(s.listR[aB + al], s.listL[c]);
-  }
-  for (int e = tid; e < EL; e += T) {
-    const int cl_ = e / nR, a = e - cl_ * nR;
-    kcL[e] = (uint8_t)idx0(s.listR[a], s.listL[cB + cl_]);
+  {
+    CellCursor<T> cur(tid, nL);
+    for (int e = tid; e < El; e += T, cur.step()) kcR[e] = (uint8_t)idx0(s.listR[aB + cur.a], s.listL[cur.c]);
+    CellCursor<T> cuc(tid, nR);  // column-major copy: (local column, row)
+    for (int e = tid; e < EL; e += T, cuc.step()) kcL[e] = (uint8_t)idx0(s.listR[cuc.c], s.listL[cB + cuc.a]);
   }
   __syncthreads();
   CMARK(2);
@@ -422,15 +420,12 @@ __device__ __forceinline__ void solve_image_cluster(const SolveArgs& args, const
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const uint8_t* tab = reinterpret_cast<const uint8_t*>(mask);
-    for (int e = tid; e < El; e += T) {
-      const int al = e / nL, c = e - al * nL;
-      kc1[e] = tab[al * kLevels + s.listL[c]];
-    }
+    CellCursor<T> cur(tid, nL);
+    for (int e = tid; e < El; e += T, cur.step()) kc1[e] = tab[cur.a * kLevels + s.listL[cur.c]];
   } else {
-    for (int e = tid; e < El; e += T) {
-      const int al = e / nL, c = e - al * nL;
-      kc1[e] = __ldg(args.idx1_tab + s.listR[aB + al] * kLevels + s.listL[c]);
-    }
+    CellCursor<T> cur(tid, nL);
+    for (int e = tid; e < El; e += T, cur.step())
+      kc1[e] = __ldg(args.idx1_tab + s.listR[aB + cur.a] * kLevels + s.listL[cur.c]);
   }
   __syncthreads();
   CMARK(6);

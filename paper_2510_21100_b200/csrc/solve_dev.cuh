@@ -325,6 +325,27 @@ __device__ __forceinline__ int mask_rank(const uint32_t* m, int a) {
 
 __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
 
+// (row, column) of the cells e = tid, tid + T, ... of an n-column matrix without a division per
+// cell (an integer division by a run-time value is ~25 instructions with two conversions)
+template <int T>
+struct CellCursor {
+  int a, c, da, dc, n;
+  __device__ CellCursor(int tid, int n_) : n(n_) {
+    a = tid / n_;
+    c = tid - a * n_;
+    da = T / n_;
+    dc = T - da * n_;
+  }
+  __device__ __forceinline__ void step() {
+    a += da;
+    c += dc;
+    if (c >= n) {
+      c -= n;
+      ++a;
+    }
+  }
+};
+
 struct RunArena {
   uint32_t* pDesc;
   double* pVal;
@@ -919,9 +940,9 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
   unsigned char* arenaG = args.cells_ws + b * (int64_t)kArenaGlobal;
   const bool keysS = E <= AB - kMaskBytes;
   uint8_t* kc = keysS ? arenaS : arenaG + (kArenaGlobal - kKeysGlobal);
-  for (int e = tid; e < E; e += T) {
-    const int a = e / nL, c = e - a * nL;
-    kc[e] = (uint8_t)idx0(s.listR[a], s.listL[c]);
+  {
+    CellCursor<T> cur(tid, nL);
+    for (int e = tid; e < E; e += T, cur.step()) kc[e] = (uint8_t)idx0(s.listR[cur.a], s.listL[cur.c]);
   }
   __syncthreads();
   RunArena A;
@@ -963,15 +984,12 @@ __device__ __forceinline__ void solve_image(const SolveArgs& args, const int64_t
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const uint8_t* tab = reinterpret_cast<const uint8_t*>(mask);
-    for (int e = tid; e < E; e += T) {
-      const int a = e / nL, c = e - a * nL;
-      kc1[e] = tab[a * kLevels + s.listL[c]];
-    }
+    CellCursor<T> cur(tid, nL);
+    for (int e = tid; e < E; e += T, cur.step()) kc1[e] = tab[cur.a * kLevels + s.listL[cur.c]];
   } else {
-    for (int e = tid; e < E; e += T) {
-      const int a = e / nL, c = e - a * nL;
-      kc1[e] = __ldg(args.idx1_tab + s.listR[a] * kLevels + s.listL[c]);
-    }
+    CellCursor<T> cur(tid, nL);
+    for (int e = tid; e < E; e += T, cur.step())
+      kc1[e] = __ldg(args.idx1_tab + s.listR[cur.a] * kLevels + s.listL[cur.c]);
   }
   // index_1 is non-decreasing along a row (b_i p_j increases with j), so row a's keys cover the
   // range [kmin_a, kmax_a]; D holds, per row, hR_a * (sum of hL over the cells of key k) for k in
